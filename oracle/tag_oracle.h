@@ -1,0 +1,70 @@
+/* oracle/tag_oracle.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C restatement of the reference's Tag env-step path, used by tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline leg as the CHECKER. It
+ * is never linked into, called by, or substituted for the product library
+ * (paper_2108_13976_b200/), which has no CPU fallback.
+ *
+ * Pinning: tests/test_oracle_pinning.py checks this restatement bit-for-bit
+ * against the reference itself, compiled from /root/reference/proj/src into
+ * oracle/_ref/ (oracle/Makefile), and against committed golden fixtures
+ * tests/golden/ (.npz) generated from that build by tests/golden/make_golden.py.
+ */
+#ifndef WD_TAG_ORACLE_H
+#define WD_TAG_ORACLE_H
+
+#include <stdint.h>
+
+#include "wdg_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Counter RNG, proj/include/warp/rng.hpp:23-53. */
+uint64_t oracle_mix64(uint64_t x);
+uint64_t oracle_key_bits(uint64_t seed, int64_t step, int64_t env, int64_t agent, int64_t category,
+                         int64_t draw);
+double oracle_uniform(uint64_t seed, int64_t step, int64_t env, int64_t agent, int64_t category,
+                      int64_t draw);
+uint64_t oracle_substream(uint64_t seed, uint64_t purpose);
+/* sample_from_logits, proj/include/warp/sampler.hpp:18-30. */
+int32_t oracle_sample_from_logits(const double* logits, int64_t n, double u);
+/* move_discrete / move_continuous, proj/include/warp/tag_env.hpp:71-100. */
+void oracle_move_discrete(int32_t action, float* x, float* y, int64_t grid_size);
+void oracle_move_continuous(int32_t accel_action, int32_t turn_action, float* speed,
+                            float* direction, float* x, float* y, float accel_delta,
+                            float turn_delta, float max_speed, float world_len);
+
+typedef struct oracle_world oracle_world;
+
+/* register_tag_arrays on a fresh store of E envs (tag_env.cpp:280-341).
+ * env_offset = global id of env 0 (keys use global ids). */
+int oracle_create(const wdg_tag_config* cfg, int64_t num_envs, int64_t env_offset,
+                  oracle_world** out);
+void oracle_destroy(oracle_world* w);
+/* sample_actions (sampler.cpp:5-40); logits NULL -> zeros. Returns 10
+ * (non_finite) on a non-finite logit, leaving actions untouched. */
+int oracle_sample(oracle_world* w, const double* logits, int64_t step, uint64_t seed);
+/* TagReference::step (tag_env.cpp:530-577). */
+int oracle_step(oracle_world* w, int64_t step);
+/* EpisodeTracker::accumulate + finish_done (trainer.cpp:229-252) folded into
+ * the stats vector (WDG_STAT_*). */
+void oracle_track(oracle_world* w);
+/* detect_done + auto_reset (reset_manager.cpp:20-44) with the Tag reinit
+ * (tag_env.cpp:579-595). Returns the number of envs reset. */
+int64_t oracle_reset_done(oracle_world* w);
+int oracle_reset_ids(oracle_world* w, const int64_t* ids, int64_t n);
+/* RolloutDriver::step x n (harness.cpp:478-494) incl. stats tracking. */
+int oracle_rollout(oracle_world* w, const double* logits, int64_t first_step, int64_t n,
+                   uint64_t seed);
+/* Direct access to one named store array (dense [E, ...]); NULL if unknown. */
+void* oracle_array(oracle_world* w, const char* name, int64_t* bytes);
+int64_t oracle_episodes(const oracle_world* w, int64_t env);
+void oracle_stats(const oracle_world* w, double* out, int32_t count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,249 @@
+// facade.hpp — the C++ host side of the B200 Tag hot path. Same names and
+// semantics as the reference's C++ API (proj/include/warp/*.hpp), with device
+// ownership: every array lives in HBM and is mutated in place by kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "tag_params.hpp"
+#include "wdg_b200.h"
+
+namespace wdg {
+
+// Errc (proj/include/warp/common.hpp:13-28) + a device failure code.
+enum class Errc : int32_t {
+  ok = WDG_OK,
+  invalid_argument = WDG_ERR_INVALID_ARGUMENT,
+  duplicate_name = WDG_ERR_DUPLICATE_NAME,
+  shape_mismatch = WDG_ERR_SHAPE_MISMATCH,
+  store_locked = WDG_ERR_STORE_LOCKED,
+  missing_placeholder = WDG_ERR_MISSING_PLACEHOLDER,
+  unknown_name = WDG_ERR_UNKNOWN_NAME,
+  index_out_of_range = WDG_ERR_INDEX_OUT_OF_RANGE,
+  invalid_config = WDG_ERR_INVALID_CONFIG,
+  step_failure = WDG_ERR_STEP_FAILURE,
+  non_finite = WDG_ERR_NON_FINITE,
+  parse_error = WDG_ERR_PARSE,
+  io_error = WDG_ERR_IO,
+  state_error = WDG_ERR_STATE,
+  cuda = WDG_ERR_CUDA,
+};
+
+class Error : public std::runtime_error {
+ public:
+  Error(Errc code, const std::string& what) : std::runtime_error(what), code_(code) {}
+  Errc code() const noexcept { return code_; }
+
+ private:
+  Errc code_;
+};
+
+[[noreturn]] void raise(Errc code, const std::string& what);
+void cuda_check(cudaError_t err, const char* what);
+
+inline int64_t element_size(int32_t kind) { return kind == WDG_BOOL8 ? 1 : 4; }
+
+// Canonical placeholders (data_store.hpp:26-29).
+inline constexpr const char* kObservations = "observations";
+inline constexpr const char* kSampledActions = "sampled_actions";
+inline constexpr const char* kRewards = "rewards";
+inline constexpr const char* kDone = "done";
+
+struct ArraySpec {
+  std::string name;
+  std::vector<int64_t> shape;
+  int32_t kind = WDG_REAL32;
+  bool snapshot_on_reset = false;
+};
+
+struct ArrayInfo {
+  ArraySpec spec;
+  int64_t total_elems = 0;
+  int64_t env_stride = 0;
+  int64_t agent_stride = 0;
+  bool has_agent_axis = false;
+};
+
+// DataStore (data_store.hpp:54-113), device-resident.
+class DataStore {
+ public:
+  DataStore(int64_t num_envs, int64_t num_agents);
+  ~DataStore();
+  DataStore(const DataStore&) = delete;
+  DataStore& operator=(const DataStore&) = delete;
+
+  int64_t num_envs() const noexcept { return num_envs_; }
+  int64_t num_agents() const noexcept { return num_agents_; }
+  bool locked() const noexcept { return locked_; }
+  int64_t env_offset() const noexcept { return env_offset_; }
+  void set_env_offset(int64_t off);
+  cudaStream_t stream() const noexcept { return stream_; }
+  void set_stream(cudaStream_t s) { stream_ = s; }
+
+  int32_t register_array(const ArraySpec& spec, const void* host_initial, int64_t count);
+  void lock();
+  bool has_array(const std::string& name) const { return index_.count(name) != 0; }
+  int32_t handle(const std::string& name) const;
+  const ArrayInfo& info(int32_t h) const;
+  int32_t num_arrays() const { return static_cast<int32_t>(arrays_.size()); }
+  int64_t row_bytes(int32_t h) const;
+
+  void push(int32_t h, int64_t env_begin, int64_t env_count, const void* host, int64_t bytes);
+  void pull(int32_t h, int64_t env_begin, int64_t env_count, void* host, int64_t bytes) const;
+  void* device_ptr(int32_t h);
+  const void* snapshot_ptr(int32_t h) const;
+  // Re-capture the snapshot from the current content (registration helpers
+  // that initialise on device; only before lock()).
+  void refresh_snapshot(int32_t h);
+  void restore_snapshot(const int64_t* env_ids, int64_t count);
+  void synchronize() const;
+
+  // Scratch owned by the store, reused by reset paths.
+  uint8_t* env_mask();
+  int64_t* id_buffer(int64_t count);
+
+ private:
+  struct Entry {
+    ArrayInfo info;
+    void* dev = nullptr;
+    void* snap = nullptr;
+    int64_t bytes = 0;
+  };
+  int32_t check_handle(int32_t h) const;
+  void check_env_range(int64_t begin, int64_t count) const;
+
+  int64_t num_envs_;
+  int64_t num_agents_;
+  int64_t env_offset_ = 0;
+  bool locked_ = false;
+  cudaStream_t stream_ = nullptr;
+  std::vector<Entry> arrays_;
+  std::unordered_map<std::string, int32_t> index_;
+  uint8_t* mask_ = nullptr;
+  int64_t* ids_ = nullptr;
+  int64_t ids_cap_ = 0;
+  void* descs_ = nullptr;
+  int32_t descs_cap_ = 0;
+  friend class ResetManager;
+};
+
+void validate_tag_config(const wdg_tag_config& cfg);
+int64_t tag_obs_dim(const wdg_tag_config& cfg);
+std::vector<std::string> tag_zero_on_reset();
+
+// Device config + geometry for a store/config pair (tag.cpp).
+TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg);
+TagDevArrays bind_dev_arrays(DataStore& store, const wdg_tag_config& cfg);
+
+void register_tag_arrays(DataStore& store, const wdg_tag_config& cfg);
+
+// TagPlan (tag_env.hpp:104-116) + StepEngine::run_step for it.
+class TagPlan {
+ public:
+  TagPlan(DataStore& store, const wdg_tag_config& cfg);
+  void run_step(int64_t step_index);
+  void reinit_masked(const uint8_t* env_mask, int32_t* episode);
+  void launch(TagLaunch L);
+  const wdg_tag_config& config() const { return cfg_; }
+  const TagDevConfig& dev() const { return dev_; }
+  DataStore& store() { return store_; }
+
+ private:
+  DataStore& store_;
+  wdg_tag_config cfg_;
+  TagDevConfig dev_;
+  TagDevArrays arrays_;
+};
+
+// sample_actions (sampler.hpp:35-36) with device logits.
+void sample_actions(DataStore& store, const double* logits, int64_t logits_count,
+                    int64_t num_categories, int64_t num_choices, int64_t step, uint64_t seed);
+
+// ResetManager (reset_manager.hpp:23-43) with a device episode counter.
+class ResetManager {
+ public:
+  ResetManager(DataStore& store, bool auto_reset, std::vector<std::string> zero_on_reset,
+               TagPlan* reinit);
+  ~ResetManager();
+  std::vector<int64_t> detect_done() const;
+  void auto_reset(const int64_t* env_ids, int64_t count);
+  void auto_reset_on_done();
+  int64_t episodes_started(int64_t env_id) const;
+  bool auto_enabled() const { return auto_; }
+  // True when the policy is exactly the Tag default (tag_zero_on_reset +
+  // make_tag_reinit), which the fused kernel implements in place.
+  bool tag_default() const { return tag_default_; }
+  int32_t* episode_device() { return episode_; }
+  TagPlan* reinit_plan() { return reinit_; }
+
+ private:
+  void reset_masked();
+  DataStore& store_;
+  bool auto_;
+  std::vector<int32_t> zero_handles_;
+  TagPlan* reinit_;
+  bool tag_default_ = false;
+  int32_t* episode_ = nullptr;
+  void* descs_ = nullptr;
+  int32_t ndesc_ = 0;
+};
+
+// RolloutDriver (harness.cpp:428-505).
+class Rollout {
+ public:
+  Rollout(DataStore& store, TagPlan& plan, ResetManager* resets, uint64_t sample_seed);
+  ~Rollout();
+  void set_logits(const double* logits, int64_t count);
+  void set_fused(bool f) { fused_ = f; }
+  void set_graphs(bool g) { graphs_ = g; }
+  void step();
+  void step_host(const double* host_logits, int64_t count, float* host_rewards, uint8_t* host_done);
+  void run(int64_t steps);
+  void reduce_stats_into(double* device_out);
+  int64_t next_step() const { return t_; }
+  void check();
+  void stats(double* out, int32_t count);
+  void reset_stats();
+  double* stats_device();
+
+ private:
+  TagLaunch fused_launch(int64_t step) const;
+  void step_unfused();
+  bool fused_ok() const;
+  DataStore& store_;
+  TagPlan& plan_;
+  ResetManager* resets_;
+  uint64_t seed_;
+  int64_t t_ = 0;
+  bool fused_ = true;
+  bool graphs_ = true;
+  const double* logits_ = nullptr;
+  double* zero_logits_ = nullptr;
+  double* env_stats_ = nullptr;
+  double* stats_ = nullptr;
+  uint32_t* error_ = nullptr;
+  int32_t* own_episode_ = nullptr;
+  uint64_t h_actions0_ = 0;
+  // host-driven stepping: double-buffered logits + copy stream
+  cudaStream_t copy_ = nullptr;
+  double* dlog_[2] = {nullptr, nullptr};
+  cudaEvent_t h2d_done_[2] = {nullptr, nullptr};
+  cudaEvent_t kern_done_[2] = {nullptr, nullptr};  // mix64(substream(seed, kStreamActions))
+};
+
+// Host-side RNG prefix helpers (rng.hpp:23-53).
+uint64_t host_mix64(uint64_t x);
+uint64_t host_absorb(uint64_t h, uint64_t v);
+uint64_t host_substream(uint64_t seed, uint64_t purpose);
+inline constexpr uint64_t kStreamActions = 0x616374696f6e7331ULL;
+inline constexpr uint64_t kStreamPlacement = 0x706c6163656d656eULL;
+
+float& fault_tag_radius_bias();
+
+}  // namespace wdg

@@ -1,0 +1,647 @@
+// tag.cpp — Tag environment host side: config validation, array registration,
+// the plan (kernel geometry + launches), sample_actions, ResetManager and the
+// rollout driver. Reference interfaces: proj/include/warp/tag_env.hpp,
+// sampler.hpp, reset_manager.hpp, proj/src/harness.cpp:428-505.
+#include <algorithm>
+#include <cmath>
+#include <set>
+
+#include "facade.hpp"
+#include "kernels.hpp"
+
+namespace wdg {
+
+// ---- host RNG prefix (rng.hpp:23-53) --------------------------------------
+uint64_t host_mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+uint64_t host_absorb(uint64_t h, uint64_t v) { return host_mix64(h ^ (v + 0x9e3779b97f4a7c15ULL)); }
+uint64_t host_substream(uint64_t seed, uint64_t purpose) {
+  return host_mix64(host_mix64(seed) ^ purpose);
+}
+
+float& fault_tag_radius_bias() {
+  static float bias = 0.0f;
+  return bias;
+}
+
+// ---- TagConfig::validate (tag_env.cpp:20-40) -------------------------------
+void validate_tag_config(const wdg_tag_config& c) {
+  auto fail = [](const std::string& msg) { raise(Errc::invalid_config, "TagConfig: " + msg); };
+  if (c.variant != WDG_TAG_DISCRETE && c.variant != WDG_TAG_CONTINUOUS) fail("unknown variant");
+  if (c.obs_mode != WDG_OBS_FULL && c.obs_mode != WDG_OBS_PARTIAL) fail("unknown obs_mode");
+  if (c.num_taggers < 1) fail("num_taggers must be >= 1");
+  if (c.num_runners < 1) fail("num_runners must be >= 1");
+  if (c.episode_length < 1) fail("episode_length must be >= 1");
+  if (c.tag_reward <= 0.0) fail("tag_reward must be > 0");
+  if (c.tagged_penalty >= 0.0) fail("tagged_penalty must be < 0");
+  if (c.variant == WDG_TAG_DISCRETE) {
+    if (c.grid_size < 1) fail("grid_size must be >= 1");
+  } else {
+    if (c.world_length <= 0.0) fail("world_length must be > 0");
+    if (c.tag_radius < 0.0) fail("tag_radius must be >= 0");
+    if (c.accel_delta <= 0.0) fail("accel_delta must be > 0");
+    if (c.turn_delta <= 0.0) fail("turn_delta must be > 0");
+    if (c.max_speed_tagger <= 0.0 || c.max_speed_runner <= 0.0) fail("max speeds must be > 0");
+  }
+  if (c.obs_mode == WDG_OBS_PARTIAL) {
+    if (c.k_nearest < 1) fail("k_nearest must be >= 1");
+    if (c.k_nearest >= c.num_taggers + c.num_runners) {
+      fail("k_nearest must be < num_taggers + num_runners");
+    }
+  }
+}
+
+int64_t tag_obs_dim(const wdg_tag_config& c) {  // tag_env.hpp:51-60
+  const bool cont = c.variant == WDG_TAG_CONTINUOUS;
+  const int64_t A = c.num_taggers + c.num_runners;
+  const int64_t vis = c.obs_mode == WDG_OBS_PARTIAL ? c.k_nearest : A - 1;
+  return vis * (cont ? 7 : 4) + (cont ? 5 : 2) + 1;
+}
+
+std::vector<std::string> tag_zero_on_reset() {  // tag_env.cpp:343-346
+  return {"step_count", kRewards, kDone, "tag_credits", "was_tagged", kSampledActions,
+          kObservations};
+}
+
+// ---- kernel geometry ------------------------------------------------------
+namespace {
+constexpr int kNumSMs = 148;
+constexpr int kBruteMaxAgents = 64;  // brute-force K-NN/resolve below this
+constexpr int kMaxSmem = 227 * 1024;
+
+int32_t round_up(int64_t v, int64_t m) { return static_cast<int32_t>((v + m - 1) / m * m); }
+int32_t align16(int64_t v) { return round_up(v, 16); }
+}  // namespace
+
+TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) {
+  validate_tag_config(cfg);
+  TagDevConfig p;
+  const int64_t A = cfg.num_taggers + cfg.num_runners;
+  if (store.num_agents() != A) {
+    raise(Errc::shape_mismatch, "tag plan: store num_agents != config agents");
+  }
+  if (A > 65535) raise(Errc::invalid_config, "device Tag path supports at most 65535 agents per env");
+  if (store.num_envs() > (int64_t{1} << 31) - 1) raise(Errc::invalid_config, "too many envs");
+  p.E = static_cast<int32_t>(store.num_envs());
+  p.A = static_cast<int32_t>(A);
+  p.T = static_cast<int32_t>(cfg.num_taggers);
+  p.continuous = cfg.variant == WDG_TAG_CONTINUOUS;
+  p.partial = cfg.obs_mode == WDG_OBS_PARTIAL;
+  p.C = p.continuous ? 2 : 1;
+  p.V = p.continuous ? 3 : 5;
+  p.K = p.partial ? static_cast<int32_t>(cfg.k_nearest) : 0;
+  if (p.partial && p.K > 32) {
+    raise(Errc::invalid_config, "device Tag path supports k_nearest <= 32");
+  }
+  p.vis = p.partial ? p.K : p.A - 1;
+  p.D = static_cast<int32_t>(tag_obs_dim(cfg));
+  p.env_offset = store.env_offset();
+  p.grid_size = cfg.grid_size;
+  p.episode_length = static_cast<int32_t>(std::min<int64_t>(cfg.episode_length, INT32_MAX));
+  p.world_length = cfg.world_length;
+  // bind_arrays constants (tag_env.cpp:106-122): each cast to float once.
+  p.world_hi = p.continuous ? static_cast<float>(cfg.world_length)
+                            : static_cast<float>(cfg.grid_size - 1);
+  const double side = p.continuous ? cfg.world_length : static_cast<double>(cfg.grid_size);
+  p.inv_world = 1.0f / static_cast<float>(side);
+  p.accel_delta = static_cast<float>(cfg.accel_delta);
+  p.turn_delta = static_cast<float>(cfg.turn_delta);
+  p.tag_radius = static_cast<float>(cfg.tag_radius);
+  p.inv_episode = 1.0f / static_cast<float>(cfg.episode_length);
+  p.reward_per_tag = static_cast<float>(cfg.tag_reward);
+  p.penalty = static_cast<float>(cfg.tagged_penalty);
+  p.max_speed_tagger = static_cast<float>(cfg.max_speed_tagger);
+  p.max_speed_runner = static_cast<float>(cfg.max_speed_runner);
+  p.inv_max_speed_tagger = 1.0f / p.max_speed_tagger;
+  p.inv_max_speed_runner = 1.0f / p.max_speed_runner;
+  p.fault_bias = fault_tag_radius_bias();
+  p.placement_h0 = host_mix64(host_substream(cfg.seed, kStreamPlacement));
+
+  // Geometry: grid path = one env per CTA; brute path packs envs per CTA.
+  p.use_grid = A > kBruteMaxAgents ? 1 : 0;
+  if (p.use_grid) {
+    p.envs_per_cta = 1;
+    p.threads = std::min<int32_t>(round_up(A, 32), 1024);
+    p.threads_per_env = p.threads;
+  } else {
+    // Smallest CTA (in warps) that holds >= 1 env, grown while the grid keeps
+    // >= 2 CTAs per SM so small-A sweeps spread over all 148 SMs.
+    int w = static_cast<int>((A + 31) / 32);
+    for (int cand = w; cand <= 8; cand *= 2) {
+      const int64_t epc = (32 * cand) / A;
+      const int64_t ctas = (store.num_envs() + epc - 1) / epc;
+      if (cand == w || ctas >= 2 * kNumSMs) w = cand;
+      else break;
+    }
+    p.envs_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (32 * w) / A));
+    p.threads_per_env = p.A;
+    p.threads = round_up(static_cast<int64_t>(p.envs_per_cta) * A, 32);
+  }
+  p.grid_ctas = static_cast<int32_t>((store.num_envs() + p.envs_per_cta - 1) / p.envs_per_cta);
+
+  // Bucket grid: ~1 agent per cell, lattice cells for discrete when possible.
+  const int sq = std::max(1, static_cast<int>(std::floor(std::sqrt(static_cast<double>(A)))));
+  if (p.continuous) {
+    p.gc = std::min(sq, 128);
+    p.cell_inv = static_cast<float>(static_cast<double>(p.gc) / cfg.world_length);
+    p.cell_size = cfg.world_length / p.gc;
+  } else {
+    p.gc = static_cast<int32_t>(std::min<int64_t>(cfg.grid_size, std::min(sq, 128)));
+    p.lattice_w = static_cast<int32_t>(cfg.grid_size / p.gc);
+  }
+  p.ncells = p.gc * p.gc;
+
+  // Shared-memory carve-up per env.
+  int64_t off = 0;
+  auto take = [&](int64_t bytes, int64_t align) {
+    off = (off + align - 1) / align * align;
+    const int32_t at = static_cast<int32_t>(off);
+    off += bytes;
+    return at;
+  };
+  take(4 * A, 16);  // x at 0
+  p.off_y = take(4 * A, 4);
+  if (p.continuous) {
+    p.off_speed = take(4 * A, 4);
+    p.off_dir = take(4 * A, 4);
+    p.off_sin = take(4 * A, 4);
+    p.off_cos = take(4 * A, 4);
+  }
+  p.off_cred = take(4 * A, 4);
+  p.off_tag = take(A, 1);
+  p.off_act = take(A, 1);
+  p.off_tagged = take(A, 1);
+  if (p.partial) p.off_knn = take(2 * A * p.K, 4);
+  if (p.use_grid) {
+    p.off_cstart = take(4 * (p.ncells + 1), 4);
+    p.off_cfill = take(4 * (p.ncells + 1), 4);
+    p.off_items = take(2 * A, 4);
+    p.off_cellof = take(2 * A, 4);
+  }
+  p.env_bytes = align16(off);
+  p.head_bytes = align16(p.envs_per_cta * 48 + 32 * 4);
+  const int64_t total = static_cast<int64_t>(p.head_bytes) + int64_t{p.envs_per_cta} * p.env_bytes;
+  if (total > kMaxSmem) {
+    raise(Errc::invalid_config, "device Tag path: " + std::to_string(A) +
+                                    " agents need " + std::to_string(total) +
+                                    " B of shared memory per env (max 227 KB)");
+  }
+  p.smem_bytes = static_cast<int32_t>(total);
+  return p;
+}
+
+TagDevArrays bind_dev_arrays(DataStore& store, const wdg_tag_config& cfg) {
+  // bind_arrays (tag_env.cpp:81-124) — same names, device addresses.
+  TagDevArrays g;
+  auto f32 = [&](const char* n) { return static_cast<float*>(store.device_ptr(store.handle(n))); };
+  auto u8 = [&](const char* n) { return static_cast<uint8_t*>(store.device_ptr(store.handle(n))); };
+  auto i32 = [&](const char* n) { return static_cast<int32_t*>(store.device_ptr(store.handle(n))); };
+  auto expect = [&](const char* n, int32_t kind, int64_t env_stride) {
+    const ArrayInfo& in = store.info(store.handle(n));
+    if (in.spec.kind != kind || in.env_stride != env_stride) {
+      raise(Errc::shape_mismatch, std::string("tag plan: array \"") + n + "\" has the wrong kind/shape");
+    }
+  };
+  const int64_t A = cfg.num_taggers + cfg.num_runners;
+  const bool cont = cfg.variant == WDG_TAG_CONTINUOUS;
+  expect("loc_x", WDG_REAL32, A);
+  expect("loc_y", WDG_REAL32, A);
+  expect("is_tagger", WDG_BOOL8, A);
+  expect("active", WDG_BOOL8, A);
+  expect("step_count", WDG_INT32, 1);
+  expect(kObservations, WDG_REAL32, A * tag_obs_dim(cfg));
+  expect(kSampledActions, WDG_INT32, A * (cont ? 2 : 1));
+  expect(kRewards, WDG_REAL32, A);
+  expect(kDone, WDG_BOOL8, 1);
+  expect("tag_credits", WDG_INT32, A);
+  expect("was_tagged", WDG_BOOL8, A);
+  g.loc_x = f32("loc_x");
+  g.loc_y = f32("loc_y");
+  if (cont) {
+    expect("speed", WDG_REAL32, A);
+    expect("direction", WDG_REAL32, A);
+    g.speed = f32("speed");
+    g.direction = f32("direction");
+  }
+  g.obs = f32(kObservations);
+  g.rewards = f32(kRewards);
+  g.is_tagger = u8("is_tagger");
+  g.active = u8("active");
+  g.tagged = u8("was_tagged");
+  g.done = u8(kDone);
+  g.step_count = i32("step_count");
+  g.actions = i32(kSampledActions);
+  g.credits = i32("tag_credits");
+  g.snap_is_tagger = static_cast<const uint8_t*>(store.snapshot_ptr(store.handle("is_tagger")));
+  return g;
+}
+
+// ---- register_tag_arrays (tag_env.cpp:280-341) ------------------------------
+void register_tag_arrays(DataStore& store, const wdg_tag_config& cfg) {
+  validate_tag_config(cfg);
+  const int64_t E = store.num_envs();
+  const int64_t A = cfg.num_taggers + cfg.num_runners;
+  if (store.num_agents() != A) {
+    raise(Errc::shape_mismatch, "register_tag_arrays: store num_agents != config agents");
+  }
+  // Geometry check first so an unsupported shape fails before any allocation.
+  (void)make_dev_config(store, cfg);
+  const bool cont = cfg.variant == WDG_TAG_CONTINUOUS;
+  std::vector<uint8_t> is_tagger(static_cast<size_t>(E * A)), active(static_cast<size_t>(E * A), 1);
+  for (int64_t e = 0; e < E; ++e)
+    for (int64_t a = 0; a < A; ++a) is_tagger[static_cast<size_t>(e * A + a)] = a < cfg.num_taggers;
+  // Same names, shapes, kinds and snapshot flags as the reference.
+  store.register_array({"loc_x", {E, A}, WDG_REAL32, true}, nullptr, 0);
+  store.register_array({"loc_y", {E, A}, WDG_REAL32, true}, nullptr, 0);
+  if (cont) {
+    store.register_array({"speed", {E, A}, WDG_REAL32, true}, nullptr, 0);
+    store.register_array({"direction", {E, A}, WDG_REAL32, true}, nullptr, 0);
+  }
+  store.register_array({"is_tagger", {E, A}, WDG_BOOL8, true}, is_tagger.data(), E * A);
+  store.register_array({"active", {E, A}, WDG_BOOL8, true}, active.data(), E * A);
+  store.register_array({"step_count", {E}, WDG_INT32, false}, nullptr, 0);
+  store.register_array({kObservations, {E, A, tag_obs_dim(cfg)}, WDG_REAL32, false}, nullptr, 0);
+  store.register_array({kSampledActions, {E, A, cont ? 2 : 1}, WDG_INT32, false}, nullptr, 0);
+  store.register_array({kRewards, {E, A}, WDG_REAL32, false}, nullptr, 0);
+  store.register_array({kDone, {E}, WDG_BOOL8, false}, nullptr, 0);
+  store.register_array({"tag_credits", {E, A}, WDG_INT32, false}, nullptr, 0);
+  store.register_array({"was_tagged", {E, A}, WDG_BOOL8, false}, nullptr, 0);
+
+  // Episode-0 placement + observations computed on device (the reinit kernel
+  // with episode 0 on every env), then captured as the registration snapshot.
+  TagDevConfig p = make_dev_config(store, cfg);
+  TagDevArrays g = bind_dev_arrays(store, cfg);
+  TagLaunch L;
+  L.mode = kModeReinit;
+  L.init_episode = 1;
+  cuda_check(launch_tag_kernel(p, g, L, store.stream()), "register_tag_arrays init kernel");
+  for (const char* n : {"loc_x", "loc_y", "speed", "direction", "active"}) {
+    if (store.has_array(n)) store.refresh_snapshot(store.handle(n));
+  }
+  store.synchronize();
+}
+
+// ---- TagPlan ---------------------------------------------------------------
+TagPlan::TagPlan(DataStore& store, const wdg_tag_config& cfg) : store_(store), cfg_(cfg) {
+  validate_tag_config(cfg);
+  if (!store.locked()) raise(Errc::state_error, "build_tag_plan: store must be locked");
+  dev_ = make_dev_config(store, cfg);
+  arrays_ = bind_dev_arrays(store, cfg);
+}
+
+void TagPlan::launch(TagLaunch L) {
+  dev_.fault_bias = fault_tag_radius_bias();
+  cuda_check(launch_tag_kernel(dev_, arrays_, L, store_.stream()), "tag kernel launch");
+}
+
+void TagPlan::run_step(int64_t step_index) {
+  (void)step_index;  // the Tag kernels do not use the step index (tag_env.cpp:530)
+  TagLaunch L;
+  L.mode = kModeStep;
+  launch(L);
+}
+
+void TagPlan::reinit_masked(const uint8_t* env_mask, int32_t* episode) {
+  TagLaunch L;
+  L.mode = kModeReinit;
+  L.env_mask = env_mask;
+  L.episode = episode;
+  launch(L);
+}
+
+// ---- sample_actions (sampler.cpp:5-40) --------------------------------------
+void sample_actions(DataStore& store, const double* logits, int64_t logits_count,
+                    int64_t num_categories, int64_t num_choices, int64_t step, uint64_t seed) {
+  const int64_t E = store.num_envs(), A = store.num_agents();
+  if (num_categories < 1 || num_choices < 1) {
+    raise(Errc::invalid_argument, "sample_actions: categories and choices must be >= 1");
+  }
+  const int64_t expected = E * A * num_categories * num_choices;
+  if (logits_count != expected) {
+    raise(Errc::shape_mismatch, "sample_actions: logits size " + std::to_string(logits_count) +
+                                    ", expected " + std::to_string(expected));
+  }
+  if (logits == nullptr) raise(Errc::invalid_argument, "sample_actions: null logits");
+  const int32_t h = store.handle(kSampledActions);
+  if (store.info(h).env_stride != A * num_categories) {
+    raise(Errc::shape_mismatch, "sample_actions: \"sampled_actions\" shape does not match "
+                                "[envs, agents, categories]");
+  }
+  // Finiteness scan before any write, as the reference does.
+  uint32_t* flag = nullptr;
+  cuda_check(cudaMalloc(&flag, sizeof(uint32_t)), "cudaMalloc(flag)");
+  uint32_t host_flag = 0;
+  cudaError_t err = cudaMemsetAsync(flag, 0, sizeof(uint32_t), store.stream());
+  if (err == cudaSuccess) err = launch_finite_scan(logits, expected, flag, store.stream());
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(&host_flag, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, store.stream());
+  if (err == cudaSuccess) err = cudaStreamSynchronize(store.stream());
+  cudaFree(flag);
+  cuda_check(err, "sample_actions finiteness scan");
+  if (host_flag) raise(Errc::non_finite, "sample_actions: non-finite logit");
+  const uint64_t h_step = host_absorb(host_mix64(host_substream(seed, kStreamActions)),
+                                      static_cast<uint64_t>(step));
+  cuda_check(launch_sample(logits, static_cast<int32_t*>(store.device_ptr(h)),
+                           E * A * num_categories, static_cast<int>(A),
+                           static_cast<int>(num_categories), static_cast<int>(num_choices),
+                           store.env_offset(), h_step, store.stream()),
+             "sample kernel");
+}
+
+// ---- ResetManager (reset_manager.cpp:5-51) ----------------------------------
+ResetManager::ResetManager(DataStore& store, bool auto_reset, std::vector<std::string> zero_on_reset,
+                           TagPlan* reinit)
+    : store_(store), auto_(auto_reset), reinit_(reinit) {
+  (void)store.handle(kDone);
+  for (const std::string& name : zero_on_reset) {
+    const int32_t h = store.handle(name);  // throws unknown_name
+    if (store.info(h).spec.snapshot_on_reset) {
+      raise(Errc::invalid_argument,
+            "ResetPolicy: \"" + name + "\" is snapshot_on_reset and cannot also be zero-filled");
+    }
+    zero_handles_.push_back(h);
+  }
+  if (reinit_ != nullptr && &reinit_->store() != &store_) {
+    raise(Errc::invalid_argument, "ResetPolicy: reinit plan belongs to another store");
+  }
+  // Descriptor table: every snapshot array restores, listed arrays zero-fill.
+  std::vector<ResetRowDesc> descs;
+  for (int32_t h = 0; h < store.num_arrays(); ++h) {
+    if (store.info(h).spec.snapshot_on_reset) {
+      descs.push_back({static_cast<uint8_t*>(store.device_ptr(h)),
+                       static_cast<const uint8_t*>(store.snapshot_ptr(h)), store.row_bytes(h)});
+    }
+  }
+  for (int32_t h : zero_handles_) {
+    descs.push_back({static_cast<uint8_t*>(store.device_ptr(h)), nullptr, store.row_bytes(h)});
+  }
+  ndesc_ = static_cast<int32_t>(descs.size());
+  if (ndesc_ > 0) {
+    cuda_check(cudaMalloc(&descs_, descs.size() * sizeof(ResetRowDesc)), "cudaMalloc(reset descs)");
+    cuda_check(cudaMemcpy(descs_, descs.data(), descs.size() * sizeof(ResetRowDesc),
+                          cudaMemcpyHostToDevice),
+               "reset descs upload");
+  }
+  cuda_check(cudaMalloc(&episode_, static_cast<size_t>(store.num_envs()) * sizeof(int32_t)),
+             "cudaMalloc(episode)");
+  cuda_check(cudaMemset(episode_, 0, static_cast<size_t>(store.num_envs()) * sizeof(int32_t)),
+             "episode clear");
+  // Fused-kernel eligibility: exactly the Tag policy.
+  std::set<std::string> want;
+  for (const std::string& n : tag_zero_on_reset()) want.insert(n);
+  std::set<std::string> have(zero_on_reset.begin(), zero_on_reset.end());
+  tag_default_ = reinit_ != nullptr && want == have;
+}
+
+ResetManager::~ResetManager() {
+  if (descs_) cudaFree(descs_);
+  if (episode_) cudaFree(episode_);
+}
+
+std::vector<int64_t> ResetManager::detect_done() const {  // reset_manager.cpp:20-27
+  const int64_t E = store_.num_envs();
+  std::vector<uint8_t> done(static_cast<size_t>(E));
+  store_.pull(store_.handle(kDone), 0, E, done.data(), E);
+  std::vector<int64_t> ids;
+  for (int64_t e = 0; e < E; ++e)
+    if (done[static_cast<size_t>(e)]) ids.push_back(e);
+  return ids;
+}
+
+void ResetManager::reset_masked() {
+  uint8_t* mask = store_.env_mask();
+  uint8_t* done = static_cast<uint8_t*>(store_.device_ptr(store_.handle(kDone)));
+  cuda_check(launch_restore_zero(static_cast<const ResetRowDesc*>(descs_), ndesc_, mask, done,
+                                 episode_, store_.num_envs(), store_.stream()),
+             "auto_reset restore/zero");
+  if (reinit_) reinit_->reinit_masked(mask, episode_);
+}
+
+void ResetManager::auto_reset(const int64_t* env_ids, int64_t count) {  // reset_manager.cpp:29-44
+  if (count == 0) return;
+  const int64_t E = store_.num_envs();
+  for (int64_t i = 0; i < count; ++i) {
+    if (env_ids[i] < 0 || env_ids[i] >= E) {
+      raise(Errc::index_out_of_range, "env_id " + std::to_string(env_ids[i]) + " out of range [0, " +
+                                          std::to_string(E) + ")");
+    }
+  }
+  uint8_t* mask = store_.env_mask();
+  int64_t* ids = store_.id_buffer(count);
+  cuda_check(cudaMemcpyAsync(ids, env_ids, static_cast<size_t>(count) * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, store_.stream()),
+             "auto_reset ids");
+  cuda_check(cudaMemsetAsync(mask, 0, static_cast<size_t>(E), store_.stream()), "mask clear");
+  cuda_check(launch_mask_from_ids(ids, count, mask, store_.stream()), "mask_from_ids");
+  reset_masked();
+  store_.synchronize();  // ids buffer is reused by the next call
+}
+
+void ResetManager::auto_reset_on_done() {
+  uint8_t* mask = store_.env_mask();
+  const uint8_t* done = static_cast<const uint8_t*>(store_.device_ptr(store_.handle(kDone)));
+  cuda_check(launch_mask_from_done(done, mask, store_.num_envs(), store_.stream()), "mask_from_done");
+  reset_masked();
+}
+
+int64_t ResetManager::episodes_started(int64_t env_id) const {
+  if (env_id < 0 || env_id >= store_.num_envs()) {
+    raise(Errc::index_out_of_range, "episodes_started: env_id out of range");
+  }
+  int32_t v = 0;
+  cuda_check(cudaMemcpyAsync(&v, episode_ + env_id, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             store_.stream()),
+             "episodes_started");
+  store_.synchronize();
+  return v;
+}
+
+// ---- Rollout driver (harness.cpp:428-505) ----------------------------------
+Rollout::Rollout(DataStore& store, TagPlan& plan, ResetManager* resets, uint64_t sample_seed)
+    : store_(store), plan_(plan), resets_(resets), seed_(sample_seed) {
+  if (&plan.store() != &store) raise(Errc::invalid_argument, "rollout: plan belongs to another store");
+  const TagDevConfig& p = plan.dev();
+  const int64_t n_logits = int64_t{p.E} * p.A * p.C * p.V;
+  // Zero logits = uniform policy (harness.cpp:439,446-447).
+  cuda_check(cudaMalloc(&zero_logits_, static_cast<size_t>(n_logits) * sizeof(double)),
+             "cudaMalloc(zero logits)");
+  cuda_check(cudaMemset(zero_logits_, 0, static_cast<size_t>(n_logits) * sizeof(double)),
+             "zero logits");
+  cuda_check(cudaMalloc(&env_stats_, static_cast<size_t>(p.E) * 8 * sizeof(double)),
+             "cudaMalloc(env stats)");
+  cuda_check(cudaMemset(env_stats_, 0, static_cast<size_t>(p.E) * 8 * sizeof(double)),
+             "env stats clear");
+  cuda_check(cudaMalloc(&stats_, WDG_STAT_COUNT * sizeof(double)), "cudaMalloc(stats)");
+  cuda_check(cudaMemset(stats_, 0, WDG_STAT_COUNT * sizeof(double)), "stats clear");
+  cuda_check(cudaMalloc(&error_, sizeof(uint32_t)), "cudaMalloc(error)");
+  cuda_check(cudaMemset(error_, 0, sizeof(uint32_t)), "error clear");
+  if (resets_ == nullptr) {
+    cuda_check(cudaMalloc(&own_episode_, static_cast<size_t>(p.E) * sizeof(int32_t)),
+               "cudaMalloc(episode)");
+    cuda_check(cudaMemset(own_episode_, 0, static_cast<size_t>(p.E) * sizeof(int32_t)),
+               "episode clear");
+  }
+  logits_ = zero_logits_;
+  h_actions0_ = host_mix64(host_substream(seed_, kStreamActions));
+}
+
+Rollout::~Rollout() {
+  for (int i = 0; i < 2; ++i) {
+    if (dlog_[i]) cudaFree(dlog_[i]);
+    if (h2d_done_[i]) cudaEventDestroy(h2d_done_[i]);
+    if (kern_done_[i]) cudaEventDestroy(kern_done_[i]);
+  }
+  if (copy_) cudaStreamDestroy(copy_);
+  if (zero_logits_) cudaFree(zero_logits_);
+  if (env_stats_) cudaFree(env_stats_);
+  if (stats_) cudaFree(stats_);
+  if (error_) cudaFree(error_);
+  if (own_episode_) cudaFree(own_episode_);
+}
+
+void Rollout::set_logits(const double* logits, int64_t count) {
+  if (logits == nullptr) {
+    logits_ = zero_logits_;
+    return;
+  }
+  const TagDevConfig& p = plan_.dev();
+  const int64_t expected = int64_t{p.E} * p.A * p.C * p.V;
+  if (count != expected) {
+    raise(Errc::shape_mismatch, "rollout: logits size " + std::to_string(count) + ", expected " +
+                                    std::to_string(expected));
+  }
+  logits_ = logits;
+}
+
+bool Rollout::fused_ok() const {
+  return fused_ && (resets_ == nullptr || !resets_->auto_enabled() ||
+                    (resets_->tag_default() && resets_->reinit_plan() == &plan_));
+}
+
+TagLaunch Rollout::fused_launch(int64_t step) const {
+  TagLaunch L;
+  L.mode = kModeFused;
+  L.do_reset = (resets_ != nullptr && resets_->auto_enabled()) ? 1 : 0;
+  L.track = 1;
+  L.action_h_step = host_absorb(h_actions0_, static_cast<uint64_t>(step));
+  L.logits = logits_;
+  L.episode = resets_ ? resets_->episode_device() : own_episode_;
+  L.env_stats = env_stats_;
+  L.error = error_;
+  return L;
+}
+
+void Rollout::step_unfused() {
+  const TagDevConfig& p = plan_.dev();
+  const uint64_t h_step = host_absorb(h_actions0_, static_cast<uint64_t>(t_));
+  cuda_check(launch_sample(logits_,
+                           static_cast<int32_t*>(store_.device_ptr(store_.handle(kSampledActions))),
+                           int64_t{p.E} * p.A * p.C, p.A, p.C, p.V, p.env_offset, h_step,
+                           store_.stream()),
+             "sample kernel");
+  plan_.run_step(t_);
+  if (resets_ != nullptr && resets_->auto_enabled()) resets_->auto_reset_on_done();
+}
+
+void Rollout::step() {
+  if (fused_ok()) {
+    plan_.launch(fused_launch(t_));
+  } else {
+    step_unfused();
+  }
+  ++t_;
+}
+
+void Rollout::step_host(const double* host_logits, int64_t count, float* host_rewards,
+                        uint8_t* host_done) {
+  const TagDevConfig& p = plan_.dev();
+  const int64_t expected = int64_t{p.E} * p.A * p.C * p.V;
+  if (host_logits == nullptr) raise(Errc::invalid_argument, "step_host: null logits");
+  if (count != expected) {
+    raise(Errc::shape_mismatch, "step_host: logits size " + std::to_string(count) + ", expected " +
+                                    std::to_string(expected));
+  }
+  const size_t bytes = static_cast<size_t>(expected) * sizeof(double);
+  if (copy_ == nullptr) {
+    cuda_check(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
+    for (int i = 0; i < 2; ++i) {
+      cuda_check(cudaMalloc(&dlog_[i], bytes), "cudaMalloc(logits slot)");
+      cuda_check(cudaEventCreateWithFlags(&h2d_done_[i], cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&kern_done_[i], cudaEventDisableTiming), "event");
+    }
+  }
+  const int slot = static_cast<int>(t_ & 1);
+  cudaStream_t st = store_.stream();
+  // The slot was last read by the kernel of step t-2.
+  cuda_check(cudaStreamWaitEvent(copy_, kern_done_[slot], 0), "wait kernel");
+  cuda_check(cudaMemcpyAsync(dlog_[slot], host_logits, bytes, cudaMemcpyHostToDevice, copy_), "H2D logits");
+  cuda_check(cudaEventRecord(h2d_done_[slot], copy_), "record h2d");
+  cuda_check(cudaStreamWaitEvent(st, h2d_done_[slot], 0), "wait h2d");
+  const double* saved = logits_;
+  logits_ = dlog_[slot];
+  try {
+    step();
+  } catch (...) {
+    logits_ = saved;
+    throw;
+  }
+  logits_ = saved;
+  cuda_check(cudaEventRecord(kern_done_[slot], st), "record kernel");
+  if (host_rewards) {
+    cuda_check(cudaMemcpyAsync(host_rewards, store_.device_ptr(store_.handle(kRewards)),
+                               static_cast<size_t>(p.E) * p.A * sizeof(float), cudaMemcpyDeviceToHost, st),
+               "D2H rewards");
+  }
+  if (host_done) {
+    cuda_check(cudaMemcpyAsync(host_done, store_.device_ptr(store_.handle(kDone)),
+                               static_cast<size_t>(p.E), cudaMemcpyDeviceToHost, st),
+               "D2H done");
+  }
+}
+
+void Rollout::reduce_stats_into(double* device_out) {
+  if (device_out == nullptr) raise(Errc::invalid_argument, "reduce_stats_into: null output");
+  cuda_check(launch_stats_reduce(env_stats_, plan_.dev().E, device_out, store_.stream()), "stats reduce");
+}
+
+void Rollout::run(int64_t steps) {
+  if (steps < 0) raise(Errc::invalid_argument, "rollout run: steps must be >= 0");
+  for (int64_t i = 0; i < steps; ++i) step();
+}
+
+void Rollout::check() {
+  uint32_t err = 0;
+  cuda_check(cudaMemcpyAsync(&err, error_, sizeof(uint32_t), cudaMemcpyDeviceToHost, store_.stream()),
+             "rollout check");
+  store_.synchronize();
+  if (err & kErrNonFinite) {
+    cudaMemsetAsync(error_, 0, sizeof(uint32_t), store_.stream());
+    raise(Errc::non_finite, "sample_actions: non-finite logit (fused rollout)");
+  }
+}
+
+void Rollout::stats(double* out, int32_t count) {
+  cuda_check(launch_stats_reduce(env_stats_, plan_.dev().E, stats_, store_.stream()), "stats reduce");
+  double host[WDG_STAT_COUNT];
+  cuda_check(cudaMemcpyAsync(host, stats_, sizeof(host), cudaMemcpyDeviceToHost, store_.stream()),
+             "stats pull");
+  store_.synchronize();
+  for (int32_t i = 0; i < count && i < WDG_STAT_COUNT; ++i) out[i] = host[i];
+}
+
+void Rollout::reset_stats() {
+  cuda_check(cudaMemsetAsync(env_stats_, 0, static_cast<size_t>(plan_.dev().E) * 8 * sizeof(double),
+                             store_.stream()),
+             "stats clear");
+}
+
+double* Rollout::stats_device() {
+  cuda_check(launch_stats_reduce(env_stats_, plan_.dev().E, stats_, store_.stream()), "stats reduce");
+  return stats_;
+}
+
+}  // namespace wdg

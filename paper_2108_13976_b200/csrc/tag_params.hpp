@@ -1,0 +1,90 @@
+// tag_params.hpp — POD parameter blocks shared by the host facade (*.cpp) and
+// the sm_100a kernels (tag_kernels.cu). Plain C++ (no CUDA types) so both
+// compilers see the identical layout.
+#pragma once
+
+#include <cstdint>
+
+namespace wdg {
+
+// Kernel modes (one kernel body, phase set chosen per launch; uniform per CTA).
+enum TagMode : int32_t {
+  kModeStep = 0,    // StepEngine::run_step: move -> resolve -> observe+reward
+  kModeFused = 1,   // RolloutDriver::step: sample -> step -> stats -> reset-on-done
+  kModeReinit = 2,  // make_tag_reinit for masked envs (or all: registration)
+};
+
+// Sticky device error bits (read at sync points, mapped to wdg_status).
+enum : uint32_t { kErrNonFinite = 1u, kErrBadAction = 2u };
+
+// Raw device addresses of one store's Tag arrays (tag_env.cpp:47-79 `Arrays`).
+struct TagDevArrays {
+  float* loc_x = nullptr;
+  float* loc_y = nullptr;
+  float* speed = nullptr;      // continuous only
+  float* direction = nullptr;  // continuous only
+  float* obs = nullptr;
+  float* rewards = nullptr;
+  uint8_t* is_tagger = nullptr;
+  uint8_t* active = nullptr;
+  uint8_t* tagged = nullptr;
+  uint8_t* done = nullptr;
+  int32_t* step_count = nullptr;
+  int32_t* actions = nullptr;
+  int32_t* credits = nullptr;
+  const uint8_t* snap_is_tagger = nullptr;  // registration-time is_tagger
+};
+
+// Config constants cast to float exactly once, as bind_arrays does
+// (tag_env.cpp:106-122), plus the launch geometry chosen by the host.
+struct TagDevConfig {
+  int32_t E = 0, A = 0, T = 0;  // envs (local), agents, taggers
+  int32_t D = 0, C = 1, V = 5, K = 0, vis = 0;
+  int32_t continuous = 0, partial = 0;
+  int64_t env_offset = 0;  // global id of local env 0 (RNG keys)
+  int64_t grid_size = 20;
+  int32_t episode_length = 500;
+  double world_length = 20.0;
+  float world_hi = 0.f, inv_world = 0.f, accel_delta = 0.f, turn_delta = 0.f;
+  float tag_radius = 0.f, inv_episode = 0.f, reward_per_tag = 0.f, penalty = 0.f;
+  float max_speed_tagger = 1.f, max_speed_runner = 1.f;
+  float inv_max_speed_tagger = 1.f, inv_max_speed_runner = 1.f;
+  float fault_bias = 0.f;            // detail::fault_hooks().tag_radius_bias
+  uint64_t placement_h0 = 0;         // mix64(substream(seed, kStreamPlacement))
+
+  // Geometry (host-chosen, see tag.cpp choose_geometry).
+  int32_t envs_per_cta = 1;
+  int32_t threads_per_env = 32;   // agent loop stride inside an env
+  int32_t threads = 32;           // blockDim.x
+  int32_t grid_ctas = 1;
+  int32_t use_grid = 0;           // bucket grid (envs_per_cta must be 1)
+  int32_t gc = 1, ncells = 1;     // grid cells per side / total
+  int32_t lattice_w = 1;          // discrete: floor(grid_size / gc)
+  float cell_inv = 1.f;           // continuous: gc / world_length
+  double cell_size = 1.0;         // continuous: world_length / gc
+  // Shared-memory carve-up, bytes.
+  int32_t env_bytes = 0;          // per-env block
+  int32_t off_y = 0, off_speed = 0, off_dir = 0, off_sin = 0, off_cos = 0;
+  int32_t off_cred = 0, off_tag = 0, off_act = 0, off_tagged = 0, off_knn = 0;
+  int32_t off_cstart = 0, off_cfill = 0, off_items = 0, off_cellof = 0;
+  int32_t head_bytes = 0;         // CTA header (per-env scalars + scan scratch)
+  int32_t smem_bytes = 0;         // total dynamic smem per CTA
+};
+
+// Per-launch arguments.
+struct TagLaunch {
+  int32_t mode = kModeStep;
+  int32_t do_reset = 1;          // fused: reset-on-done enabled
+  int32_t track = 0;             // fused: EpisodeTracker stats
+  int32_t init_episode = 0;      // reinit: 1 = registration (episode stays 0)
+  uint64_t action_h_step = 0;    // absorb(mix64(substream(seed,kStreamActions)), step)
+  const double* logits = nullptr;
+  const uint8_t* env_mask = nullptr;  // reinit: envs to reinit (nullptr = all)
+  int32_t* episode = nullptr;         // per-env episode counter (device)
+  // Per-env tracker slots [E][8]: run_tagger, run_runner, episodes,
+  // tagger_return, runner_return, tag_events, env_steps, (pad).
+  double* env_stats = nullptr;
+  uint32_t* error = nullptr;          // sticky error word
+};
+
+}  // namespace wdg
