@@ -4,6 +4,7 @@
 // sampler.hpp, reset_manager.hpp, proj/src/harness.cpp:428-505.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <set>
 
 #include "facade.hpp"
@@ -124,8 +125,12 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   // Geometry: grid path = one env per CTA; brute path packs envs per CTA.
   p.use_grid = A > kBruteMaxAgents ? 1 : 0;
   if (p.use_grid) {
+    // One env per CTA, one thread per agent up to the CTA cap (larger A
+    // loops). WDG_TPE_MAX overrides the cap (tuning experiments).
+    int cap = 1024;
+    if (const char* env = std::getenv("WDG_TPE_MAX")) cap = std::clamp(std::atoi(env), 32, 1024) / 32 * 32;
     p.envs_per_cta = 1;
-    p.threads = std::min<int32_t>(round_up(A, 32), 1024);
+    p.threads = std::min<int32_t>(round_up(A, 32), cap);
     p.threads_per_env = p.threads;
   } else {
     // Smallest CTA (in warps) that holds >= 1 env, grown while the grid keeps
@@ -152,8 +157,15 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   } else {
     p.gc = static_cast<int32_t>(std::min<int64_t>(cfg.grid_size, std::min(sq, 128)));
     p.lattice_w = static_cast<int32_t>(cfg.grid_size / p.gc);
+    p.lattice = p.gc == cfg.grid_size ? 1 : 0;
   }
   p.ncells = p.gc * p.gc;
+  // Observation rows staged per warp in shared memory when a row is narrow.
+  const int64_t nwarps = p.threads / 32;
+  const int64_t stage_bytes = nwarps * 32 * int64_t{p.D} * 4;
+  p.stage_obs = (p.D <= 64 && stage_bytes <= 112 * 1024) ? 1 : 0;
+  if (const char* env = std::getenv("WDG_STAGE_OBS")) p.stage_obs = p.stage_obs && std::atoi(env) != 0;
+  p.stage_floats = 32 * p.D;
 
   // Shared-memory carve-up per env.
   int64_t off = 0;
@@ -175,7 +187,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   p.off_tag = take(A, 1);
   p.off_act = take(A, 1);
   p.off_tagged = take(A, 1);
-  if (p.partial) p.off_knn = take(2 * A * p.K, 4);
+  if (p.partial && !p.stage_obs) p.off_knn = take(2 * A * p.K, 4);
   if (p.use_grid) {
     p.off_cstart = take(4 * (p.ncells + 1), 4);
     p.off_cfill = take(4 * (p.ncells + 1), 4);
@@ -183,8 +195,13 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
     p.off_cellof = take(2 * A, 4);
   }
   p.env_bytes = align16(off);
-  p.head_bytes = align16(p.envs_per_cta * 48 + 32 * 4);
-  const int64_t total = static_cast<int64_t>(p.head_bytes) + int64_t{p.envs_per_cta} * p.env_bytes;
+  // CTA header: per-env scalars + 64 doubles of warp scratch (scan / sums).
+  p.head_bytes = align16(p.envs_per_cta * 48 + 64 * 8);
+  int64_t total = static_cast<int64_t>(p.head_bytes) + int64_t{p.envs_per_cta} * p.env_bytes;
+  if (p.stage_obs) {
+    p.off_stage = static_cast<int32_t>(align16(total));
+    total = p.off_stage + stage_bytes;
+  }
   if (total > kMaxSmem) {
     raise(Errc::invalid_config, "device Tag path: " + std::to_string(A) +
                                     " agents need " + std::to_string(total) +

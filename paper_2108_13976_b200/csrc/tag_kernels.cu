@@ -121,7 +121,7 @@ struct EnvScalars {
   int32_t episode;
   int32_t tags;
   int32_t live;
-  int32_t did_reset;
+  int32_t lattice_ok;  // all positions integral (discrete lattice K-NN valid)
   int32_t pad;
   double ret_tagger;
   double ret_runner;
@@ -166,6 +166,19 @@ __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
   return s;
 }
 
+// ---- lattice shells (discrete K-NN) ------------------------------------------
+// All lattice offsets (dx, dy) with dx^2+dy^2 <= kShellR2, sorted by d2 and
+// grouped into shells of equal d2. Visiting shells in order makes the K-NN
+// search stop as soon as the K-th best is strictly closer than the next shell.
+constexpr int kShellR = 12;
+constexpr int kShellR2 = kShellR * kShellR;
+constexpr int kMaxShellOffsets = 4 * kShellR2 + 4 * kShellR + 1;  // >= #offsets in the disk
+constexpr int kMaxShells = kShellR2 + 2;
+__constant__ int16_t c_shell_off[kMaxShellOffsets];  // (dx + 64) | (dy + 64) << 8
+__constant__ int16_t c_shell_begin[kMaxShells + 1];
+__constant__ int16_t c_shell_d2[kMaxShells];
+__constant__ int32_t c_num_shells;
+
 // ---- bucket grid (NeighborGrid semantics, neighbor_grid.hpp:11-111) -------
 template <bool CONT>
 __device__ __forceinline__ int cell_coord(float v, const TagDevConfig& p) {
@@ -176,7 +189,9 @@ __device__ __forceinline__ int cell_coord(float v, const TagDevConfig& p) {
     int iv = static_cast<int>(floorf(v));
     const int g = static_cast<int>(p.grid_size);
     iv = iv < 0 ? 0 : (iv > g - 1 ? g - 1 : iv);
-    return static_cast<int>((static_cast<int64_t>(iv) * p.gc) / g);
+    if (p.lattice) return iv;
+    return static_cast<int>((static_cast<uint32_t>(iv) * static_cast<uint32_t>(p.gc)) /
+                            static_cast<uint32_t>(g));
   }
 }
 
@@ -243,8 +258,9 @@ __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch
 // ---- exact top-K under the (d2, index) total order ------------------------
 // Same selection as select_k_nearest_brute (tag_env.cpp:225-237) and
 // NeighborGrid::k_nearest (neighbor_grid.hpp:62-111): unique because the
-// order is total, so any visiting order gives the identical list.
-template <int MAXK>
+// order is total, so any visiting order gives the identical list. EXACT:
+// k == MAXK at compile time (no runtime guards in the insertion network).
+template <int MAXK, bool EXACT>
 struct TopK {
   float d[MAXK];
   int i[MAXK];
@@ -252,7 +268,7 @@ struct TopK {
   int wi;
   int k;
   __device__ __forceinline__ void init(int kk) {
-    k = kk;
+    k = EXACT ? MAXK : kk;
 #pragma unroll
     for (int t = 0; t < MAXK; ++t) {
       d[t] = __int_as_float(0x7f800000);
@@ -262,12 +278,15 @@ struct TopK {
     wi = 0x7fffffff;
   }
   __device__ __forceinline__ bool full() const { return wi != 0x7fffffff; }
+  __device__ __forceinline__ bool admits(float dd, int j) const {
+    return dd < wd || (dd == wd && j < wi);
+  }
   __device__ __forceinline__ void consider(float dd, int j) {
-    if (!(dd < wd || (dd == wd && j < wi))) return;
+    if (!admits(dd, j)) return;
     bool placed = false;
 #pragma unroll
     for (int t = MAXK - 1; t >= 0; --t) {
-      if (t < k) {
+      if (EXACT || t < k) {
         const bool shift = t > 0 && (dd < d[t - 1] || (dd == d[t - 1] && j < i[t - 1]));
         if (shift) {
           d[t] = d[t - 1];
@@ -279,11 +298,16 @@ struct TopK {
         }
       }
     }
+    if (EXACT) {
+      wd = d[MAXK - 1];
+      wi = i[MAXK - 1];
+    } else {
 #pragma unroll
-    for (int t = 0; t < MAXK; ++t) {
-      if (t == k - 1) {
-        wd = d[t];
-        wi = i[t];
+      for (int t = 0; t < MAXK; ++t) {
+        if (t == k - 1) {
+          wd = d[t];
+          wi = i[t];
+        }
       }
     }
   }
@@ -295,24 +319,17 @@ __device__ __forceinline__ float d2_of(float ax, float ay, float bx, float by) {
   return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
 }
 
-template <bool CONT, bool GRID, int MAXK>
-__device__ void knn_agent(const EnvSmem& s, const TagDevConfig& p, int a, TopK<MAXK>& top) {
+// Generic ring search over the bucket grid (continuous / non-lattice).
+template <bool CONT, int MAXK, bool EXACT>
+__device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<MAXK, EXACT>& top) {
   const float sx = s.x[a], sy = s.y[a];
-  top.init(p.K);
-  if (!GRID) {
-    for (int j = 0; j < p.A; ++j) {
-      if (j == a) continue;
-      top.consider(d2_of(sx, sy, s.x[j], s.y[j]), j);
-    }
-    return;
-  }
   const int gc = p.gc;
   const int cx = cell_coord<CONT>(sx, p), cy = cell_coord<CONT>(sy, p);
   const int maxr = max(max(cx, gc - 1 - cx), max(cy, gc - 1 - cy));
   for (int r = 0; r <= maxr; ++r) {
     if (r > 0 && top.full()) {
-      // Every point in rings >= r is farther than the bound below (SURVEY.md
-      // §8a a6; cf. the reference's ring margin, neighbor_grid.hpp:90-96).
+      // Every point in rings >= r is farther than this bound (SURVEY.md §8a
+      // a6; cf. the reference's ring margin, neighbor_grid.hpp:90-96).
       float lb2;
       if (CONT) {
         const double lb = fmax(0.0, (r - 1) - 1e-3) * p.cell_size;
@@ -326,8 +343,8 @@ __device__ void knn_agent(const EnvSmem& s, const TagDevConfig& p, int a, TopK<M
     const int y0 = cy - r, y1 = cy + r, x0 = cx - r, x1 = cx + r;
     for (int gy = max(y0, 0); gy <= min(y1, gc - 1); ++gy) {
       const bool edge = (gy == y0 || gy == y1);
-      const int step = edge ? 1 : (x1 - x0);
-      for (int gx = x0; gx <= x1; gx += (step > 0 ? step : 1)) {
+      const int step = edge ? 1 : max(x1 - x0, 1);
+      for (int gx = x0; gx <= x1; gx += step) {
         if (gx < 0 || gx >= gc) continue;
         const int c = gy * gc + gx;
         const int e = s.cstart[c + 1];
@@ -339,6 +356,57 @@ __device__ void knn_agent(const EnvSmem& s, const TagDevConfig& p, int a, TopK<M
       }
     }
   }
+}
+
+// Discrete lattice search: shells of equal integer d2 in increasing order.
+// Candidates need no coordinate reads (d2 is the shell's). Falls back to the
+// ring search if the precomputed disk is exhausted (very sparse envs).
+template <int MAXK, bool EXACT>
+__device__ void knn_lattice(const EnvSmem& s, const TagDevConfig& p, int a, TopK<MAXK, EXACT>& top) {
+  const int cx = static_cast<int>(s.x[a]), cy = static_cast<int>(s.y[a]);
+  const int g = p.gc;
+  const int ns = c_num_shells;
+  for (int sh = 0; sh < ns; ++sh) {
+    const float d2s = static_cast<float>(c_shell_d2[sh]);
+    if (top.full() && top.wd < d2s) return;
+    const int ob = c_shell_begin[sh], oe = c_shell_begin[sh + 1];
+    for (int o = ob; o < oe; ++o) {
+      const int packed = c_shell_off[o];
+      const int gx = cx + (packed & 0xff) - 64;
+      const int gy = cy + ((packed >> 8) & 0xff) - 64;
+      if (static_cast<unsigned>(gx) >= static_cast<unsigned>(g) ||
+          static_cast<unsigned>(gy) >= static_cast<unsigned>(g))
+        continue;
+      const int c = gy * g + gx;
+      const int e = s.cstart[c + 1];
+      for (int t = s.cstart[c]; t < e; ++t) {
+        const int j = s.items[t];
+        if (j != a) top.consider(d2s, j);
+      }
+    }
+  }
+  if (top.full() && top.wd <= static_cast<float>(kShellR2)) return;
+  top.init(p.K);
+  knn_rings<false, MAXK, EXACT>(s, p, a, top);
+}
+
+template <bool CONT, bool GRID, int MAXK, bool EXACT>
+__device__ __forceinline__ void knn_agent(const EnvSmem& s, const TagDevConfig& p, int a,
+                                          bool lattice_ok, TopK<MAXK, EXACT>& top) {
+  top.init(p.K);
+  if (!GRID) {
+    const float sx = s.x[a], sy = s.y[a];
+    for (int j = 0; j < p.A; ++j) {
+      if (j == a) continue;
+      top.consider(d2_of(sx, sy, s.x[j], s.y[j]), j);
+    }
+    return;
+  }
+  if (!CONT && lattice_ok) {
+    knn_lattice<MAXK, EXACT>(s, p, a, top);
+    return;
+  }
+  knn_rings<CONT, MAXK, EXACT>(s, p, a, top);
 }
 
 // Tag resolution for one active runner: resolve kernel (tag_env.cpp:403-456)
@@ -387,7 +455,12 @@ __device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn) {
   return best;
 }
 
-// One observation element (write_obs_row, tag_env.cpp:165-212).
+__device__ __forceinline__ float inv_ms(const TagDevConfig& p, int j) {
+  return j < p.T ? p.inv_max_speed_tagger : p.inv_max_speed_runner;
+}
+
+// One observation element (write_obs_row, tag_env.cpp:165-212) — used by the
+// cooperative (non-staged) writer for wide rows.
 template <bool CONT, bool PARTIAL>
 __device__ __forceinline__ float obs_value(const EnvSmem& s, const TagDevConfig& p,
                                            int32_t step_count, int a, int f) {
@@ -403,8 +476,7 @@ __device__ __forceinline__ float obs_value(const EnvSmem& s, const TagDevConfig&
       case 1: return __fmul_rn(__fsub_rn(s.y[j], s.y[a]), p.inv_world);
       case 2: return s.tag[j] ? 1.0f : 0.0f;
       case 3: return s.act[j] ? 1.0f : 0.0f;
-      case 4:
-        return __fmul_rn(s.sp[j], j < p.T ? p.inv_max_speed_tagger : p.inv_max_speed_runner);
+      case 4: return __fmul_rn(s.sp[j], inv_ms(p, j));
       case 5: return s.sn[j];
       default: return s.cs[j];
     }
@@ -413,11 +485,52 @@ __device__ __forceinline__ float obs_value(const EnvSmem& s, const TagDevConfig&
   if (t == 0) return __fmul_rn(s.x[a], p.inv_world);
   if (t == 1) return __fmul_rn(s.y[a], p.inv_world);
   if (CONT) {
-    if (t == 2) return __fmul_rn(s.sp[a], a < p.T ? p.inv_max_speed_tagger : p.inv_max_speed_runner);
+    if (t == 2) return __fmul_rn(s.sp[a], inv_ms(p, a));
     if (t == 3) return s.sn[a];
     if (t == 4) return s.cs[a];
   }
   return __fmul_rn(static_cast<float>(step_count), p.inv_episode);
+}
+
+// Writes one agent's full observation row (write_obs_row) to `out`
+// (a warp staging buffer in shared memory). `nb(n)` yields the n-th visible
+// neighbour.
+template <bool CONT, class NB>
+__device__ __forceinline__ void write_row(const EnvSmem& s, const TagDevConfig& p, int32_t step_count,
+                                          int a, float* out, NB nb) {
+  if (!s.act[a]) {
+    for (int f = 0; f < p.D; ++f) out[f] = 0.0f;
+    return;
+  }
+  const float sx = s.x[a], sy = s.y[a];
+  const float iw = p.inv_world;
+  int o = 0;
+  for (int n = 0; n < p.vis; ++n) {
+    const int j = nb(n);
+    out[o + 0] = __fmul_rn(__fsub_rn(s.x[j], sx), iw);
+    out[o + 1] = __fmul_rn(__fsub_rn(s.y[j], sy), iw);
+    out[o + 2] = s.tag[j] ? 1.0f : 0.0f;
+    out[o + 3] = s.act[j] ? 1.0f : 0.0f;
+    if (CONT) {
+      out[o + 4] = __fmul_rn(s.sp[j], inv_ms(p, j));
+      out[o + 5] = s.sn[j];
+      out[o + 6] = s.cs[j];
+      o += 7;
+    } else {
+      o += 4;
+    }
+  }
+  out[o + 0] = __fmul_rn(sx, iw);
+  out[o + 1] = __fmul_rn(sy, iw);
+  if (CONT) {
+    out[o + 2] = __fmul_rn(s.sp[a], inv_ms(p, a));
+    out[o + 3] = s.sn[a];
+    out[o + 4] = s.cs[a];
+    o += 5;
+  } else {
+    o += 2;
+  }
+  out[o] = __fmul_rn(static_cast<float>(step_count), p.inv_episode);
 }
 
 // sinf/cosf evaluated in f64 and rounded once: the correctly-rounded value
@@ -426,12 +539,23 @@ __device__ __forceinline__ float obs_value(const EnvSmem& s, const TagDevConfig&
 __device__ __forceinline__ float sin_ref(float v) { return __double2float_rn(sin(static_cast<double>(v))); }
 __device__ __forceinline__ float cos_ref(float v) { return __double2float_rn(cos(static_cast<double>(v))); }
 
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // ---- the env-step kernel --------------------------------------------------
-template <bool CONT, bool PARTIAL, bool GRID, int MAXK>
+// Thread layout: tid = le * tpe + lt (le = env slot in the CTA, lt = lane in
+// the env). Per-agent loops run over `base` in warp-uniform steps so warp
+// collectives are legal; agent a = base + lt.
+template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT>
 __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, const TagDevArrays g,
                                                        const TagLaunch L) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
   const int tpe = p.threads_per_env;
   const int le = tid / tpe;
   const int lt = tid - le * tpe;
@@ -439,10 +563,15 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
   const bool env_ok = le < p.envs_per_cta && e < p.E;
   const int mode = L.mode;
   const int A = p.A;
+  const bool single = p.envs_per_cta == 1;  // CTA == one env: warp collectives are per env
 
   bool live = env_ok;
   if (mode == kModeReinit && L.env_mask != nullptr && env_ok) live = L.env_mask[e] != 0;
-  if (p.envs_per_cta == 1 && !live) return;  // CTA-uniform
+  if (single) {  // CTA-uniform early exit: decided by the CTA's env, not by this thread
+    const int64_t e0 = blockIdx.x;
+    const bool l0 = e0 < p.E && !(mode == kModeReinit && L.env_mask != nullptr && !L.env_mask[e0]);
+    if (!l0) return;
+  }
 
   EnvScalars* scal = reinterpret_cast<EnvScalars*>(smem);
   int* scratch = reinterpret_cast<int*>(smem + p.envs_per_cta * sizeof(EnvScalars));
@@ -451,11 +580,15 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
   const int64_t ga = e * A;
 
   // Phase 0: stage the env's agent state in shared memory.
+  bool integral = true;
   if (live) {
     for (int a = lt; a < A; a += tpe) {
       if (mode != kModeReinit) {
-        s.x[a] = g.loc_x[ga + a];
-        s.y[a] = g.loc_y[ga + a];
+        const float x = g.loc_x[ga + a], y = g.loc_y[ga + a];
+        s.x[a] = x;
+        s.y[a] = y;
+        integral &= (x == truncf(x)) && (y == truncf(y)) && x >= 0.0f && y >= 0.0f &&
+                    x <= p.world_hi && y <= p.world_hi;
         s.act[a] = g.active[ga + a];
         if (CONT) {
           s.sp[a] = g.speed[ga + a];
@@ -473,7 +606,7 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
       sc.episode = (L.episode != nullptr && !(mode == kModeReinit && L.init_episode)) ? L.episode[e] : 0;
       sc.tags = 0;
       sc.live = 1;
-      sc.did_reset = 0;
+      sc.lattice_ok = 1;
       sc.ret_tagger = 0.0;
       sc.ret_runner = 0.0;
     }
@@ -481,7 +614,9 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     sc.live = 0;
   }
   __syncthreads();
+  if (!CONT && GRID && !integral) sc.lattice_ok = 0;  // benign same-value race
 
+  bool reset_now = false;
   if (mode != kModeReinit) {
     // Phase 1: sample (fused) + move (apply_move, tag_env.cpp:148-160).
     if (live) {
@@ -541,19 +676,29 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     // Phase 2: bucket grid over post-move positions (NeighborGrid::build).
     if (GRID) build_grid<CONT>(s, p, scratch);
 
-    // Phase 3: resolve tags (tag_env.cpp:403-456).
-    if (live) {
-      for (int a = lt; a < A; a += tpe) {
-        if (s.tag[a] || !s.act[a]) continue;
-        const int best = find_tagger<CONT, GRID>(s, p, a);
-        if (best >= 0) {
-          s.act[a] = 0;
-          s.tagged[a] = 1;
-          atomicAdd(&s.cred[best], 1);
-          atomicAdd(&sc.tags, 1);
-        } else {
-          atomicAdd(&sc.runners_left, 1);
+    // Phase 3: resolve tags (tag_env.cpp:403-456). Counts are warp-aggregated
+    // when the CTA is one env.
+    for (int base = 0; base < A; base += tpe) {
+      const int a = base + lt;
+      const bool valid = live && a < A;
+      const bool runner = valid && !s.tag[a] && s.act[a];
+      const int best = runner ? find_tagger<CONT, GRID>(s, p, a) : -1;
+      if (best >= 0) {
+        s.act[a] = 0;
+        s.tagged[a] = 1;
+        atomicAdd(&s.cred[best], 1);
+      }
+      const bool alive = runner && best < 0;
+      if (single) {
+        const unsigned m_alive = __ballot_sync(0xffffffffu, alive);
+        const unsigned m_tag = __ballot_sync(0xffffffffu, best >= 0);
+        if (lane == 0 && (m_alive | m_tag)) {
+          if (m_alive) atomicAdd(&scal[0].runners_left, __popc(m_alive));
+          if (m_tag) atomicAdd(&scal[0].tags, __popc(m_tag));
         }
+      } else {
+        if (alive) atomicAdd(&sc.runners_left, 1);
+        if (best >= 0) atomicAdd(&sc.tags, 1);
       }
     }
     __syncthreads();
@@ -565,9 +710,10 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     __syncthreads();
 
     // Phase 4: rewards (write_rewards_row, tag_env.cpp:252-259) + tracker.
+    reset_now = live && mode == kModeFused && L.do_reset && sc.done;
+    const bool track = mode == kModeFused && L.track;
+    double rt = 0.0, rr = 0.0;
     if (live) {
-      const bool reset_now = mode == kModeFused && L.do_reset && sc.done;
-      double rt = 0.0, rr = 0.0;
       for (int a = lt; a < A; a += tpe) {
         const float r = s.tag[a] ? __fmul_rn(p.reward_per_tag, static_cast<float>(s.cred[a]))
                                  : (s.tagged[a] ? p.penalty : 0.0f);
@@ -576,18 +722,39 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
         g.credits[ga + a] = reset_now ? 0 : s.cred[a];
         g.tagged[ga + a] = reset_now ? 0 : s.tagged[a];
       }
-      if (mode == kModeFused && L.track) {
+    }
+    if (track) {
+      if (single) {
+        // warp sums -> per-warp slots in `scratch` (as doubles) -> one adder
+        rt = warp_sum(rt);
+        rr = warp_sum(rr);
+        double* slots = reinterpret_cast<double*>(scratch);  // 2 x 32 doubles fit in head
+        if (lane == 0) {
+          slots[warp] = rt;
+          slots[32 + warp] = rr;
+        }
+      } else if (live) {
         atomicAdd(&sc.ret_tagger, rt);
         atomicAdd(&sc.ret_runner, rr);
       }
     }
     __syncthreads();
-    if (live && lt == 0 && mode == kModeFused && L.track) {
+    if (live && lt == 0 && track) {
       // EpisodeTracker::accumulate / finish_done (trainer.cpp:229-252); per-env
       // slots, no atomics: [run_t, run_r, episodes, ret_t, ret_r, tags, steps].
+      double st = sc.ret_tagger, sr = sc.ret_runner;
+      if (single) {
+        const double* slots = reinterpret_cast<const double*>(scratch);
+        st = 0.0;
+        sr = 0.0;
+        for (int w = 0; w < (blockDim.x >> 5); ++w) {
+          st += slots[w];
+          sr += slots[32 + w];
+        }
+      }
       double* es = L.env_stats + e * 8;
-      const double run_t = es[0] + sc.ret_tagger;
-      const double run_r = es[1] + sc.ret_runner;
+      const double run_t = es[0] + st;
+      const double run_r = es[1] + sr;
       es[5] += sc.tags;
       es[6] += 1.0;
       if (sc.done) {
@@ -605,9 +772,9 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
 
   // Phase 5: (re)placement — fused reset-on-done or reinit (place_env,
   // tag_env.cpp:261-273; place_agent :130-146).
-  const bool place = live && (mode == kModeReinit || (mode == kModeFused && L.do_reset && sc.done));
+  const bool place = live && (mode == kModeReinit || reset_now);
+  const int episode = mode == kModeFused ? sc.episode + 1 : sc.episode;
   if (place) {
-    const int episode = mode == kModeFused ? sc.episode + 1 : sc.episode;
     const uint64_t h_ep = absorb(p.placement_h0, static_cast<uint64_t>(static_cast<int64_t>(episode)));
     const uint64_t h_env = absorb(h_ep, static_cast<uint64_t>(p.env_offset + e));
     for (int a = lt; a < A; a += tpe) {
@@ -640,14 +807,14 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
         if (CONT) g.actions[(ga + a) * p.C + 1] = 0;
       }
     }
-    if (lt == 0) {
-      sc.step_count = 0;
-      sc.done = 0;
-      sc.episode = episode;
-      sc.did_reset = 1;
-    }
   }
-  __syncthreads();
+  __syncthreads();  // everyone has read sc.* above before it is rewritten
+  if (place && lt == 0) {
+    sc.step_count = 0;
+    sc.done = 0;
+    sc.episode = episode;
+    sc.lattice_ok = 1;  // placement is integral
+  }
 
   // Phase 6: observation inputs. Continuous: fill_sincos (tag_env.cpp:214-221).
   if (CONT && live) {
@@ -656,89 +823,105 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
       s.cs[a] = cos_ref(s.dir[a]);
     }
   }
-  if (GRID && PARTIAL && (mode == kModeReinit || scal[0].did_reset)) {
-    // positions changed by placement: rebuild (CTA == one env on this path)
+  // single-env CTA: `place` is CTA-uniform here (every thread has le == 0)
+  if (GRID && PARTIAL && single && place) {
     __syncthreads();
     build_grid<CONT>(s, p, scratch);
   }
-  if (PARTIAL && live) {
-    for (int a = lt; a < A; a += tpe) {
-      if (!s.act[a]) continue;
-      TopK<MAXK> top;
-      knn_agent<CONT, GRID, MAXK>(s, p, a, top);
+  __syncthreads();
+  const bool lattice_ok = !CONT && GRID && scal[0].lattice_ok;
+
+  // Phase 7: K-NN + observation rows (write_obs_row, tag_env.cpp:165-212).
+  const int64_t cta_env0 = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
+  const int n_envs = static_cast<int>(min(static_cast<int64_t>(p.envs_per_cta), p.E - cta_env0));
+  const int D = p.D;
+  float* cta_out = g.obs + cta_env0 * A * D;
+  if (p.stage_obs) {
+    // Each thread builds its agent's row in a per-warp staging buffer; the
+    // warp then streams the contiguous block of its rows with 16-byte stores.
+    float* stage = reinterpret_cast<float*>(smem + p.off_stage) + warp * p.stage_floats;
+    const bool vec = ((static_cast<int64_t>(p.envs_per_cta) * A * D) & 3) == 0;
+    for (int base = 0; base < A; base += tpe) {
+      const int a = base + lt;
+      const bool valid = live && a < A;
+      if (valid) {
+        float* row = stage + lane * D;
+        if (PARTIAL && s.act[a]) {
+          TopK<MAXK, EXACT> top;
+          knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top);
+          write_row<CONT>(s, p, sc.step_count, a, row, [&](int n) {
+            int j = top.i[0];
 #pragma unroll
-      for (int t = 0; t < MAXK; ++t) {
-        if (t < p.K) s.knn[a * p.K + t] = static_cast<uint16_t>(top.i[t]);
+            for (int t = 1; t < MAXK; ++t)
+              if (t == n) j = top.i[t];
+            return j;
+          });
+        } else {
+          write_row<CONT>(s, p, sc.step_count, a, row, [&](int n) { return n < a ? n : n + 1; });
+        }
+      }
+      __syncwarp();
+      // Rows of this warp in CTA-row space (row = le * A + a); when the valid
+      // lanes form a prefix (always, except masked reinit of packed envs) the
+      // rows are one contiguous block -> coalesced 16-byte streaming stores.
+      const int myrow = env_ok ? le * A + a : -1;
+      const int row0 = __shfl_sync(0xffffffffu, myrow, 0);
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      if ((vmask & (vmask + 1u)) == 0u) {
+        const int nf = __popc(vmask) * D;
+        float* dst = cta_out + static_cast<int64_t>(row0) * D;
+        if (vec && ((static_cast<int64_t>(row0) * D) & 3) == 0) {
+          const int nv = nf >> 2;
+          for (int v = lane; v < nv; v += 32)
+            __stcs(reinterpret_cast<float4*>(dst) + v, reinterpret_cast<const float4*>(stage)[v]);
+          for (int f = (nv << 2) + lane; f < nf; f += 32) __stcs(dst + f, stage[f]);
+        } else {
+          for (int f = lane; f < nf; f += 32) __stcs(dst + f, stage[f]);
+        }
+      } else if (valid) {
+        float* dst = cta_out + static_cast<int64_t>(myrow) * D;
+        for (int f = 0; f < D; ++f) __stcs(dst + f, stage[lane * D + f]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // Wide rows (full obs, large A): K-NN into smem, then the CTA writes its
+    // contiguous [envs, A, D] block cooperatively (coalesced).
+    if (PARTIAL && live) {
+      for (int a = lt; a < A; a += tpe) {
+        if (!s.act[a]) continue;
+        TopK<MAXK, EXACT> top;
+        knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top);
+#pragma unroll
+        for (int t = 0; t < MAXK; ++t) {
+          if (t < p.K) s.knn[a * p.K + t] = static_cast<uint16_t>(top.i[t]);
+        }
       }
     }
-  }
-  __syncthreads();
-
-  // Phase 7: observations — the CTA's [envs, A, D] block written as one
-  // contiguous, coalesced stream (16-byte streaming stores when aligned).
-  {
-    const int64_t cta_env0 = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
-    const int n_envs = static_cast<int>(min(static_cast<int64_t>(p.envs_per_cta), p.E - cta_env0));
-    const int D = p.D;
+    __syncthreads();
     const int64_t n = static_cast<int64_t>(n_envs) * A * D;
-    float* out = g.obs + cta_env0 * A * D;
     const int nthr = blockDim.x;
     const uint8_t* base0 = smem + p.head_bytes;
     auto value = [&](int row, int f) -> float {
       int lenv = 0, a = row;
-      if (p.envs_per_cta > 1) {
+      if (!single) {
         lenv = row / A;
         a = row - lenv * A;
       }
       const EnvSmem es = carve(const_cast<uint8_t*>(base0) + lenv * p.env_bytes, p);
       return obs_value<CONT, PARTIAL>(es, p, scal[lenv].step_count, a, f);
     };
-    auto row_live = [&](int row) -> bool {
-      if (p.envs_per_cta == 1) return true;
-      return scal[row / A].live != 0;
-    };
-    if (((static_cast<int64_t>(A) * D) & 3) == 0) {
-      const int64_t nv = n >> 2;
-      float4* out4 = reinterpret_cast<float4*>(out);
-      int64_t idx = static_cast<int64_t>(tid) * 4;
-      int row = static_cast<int>(idx / D);
-      int f = static_cast<int>(idx - static_cast<int64_t>(row) * D);
-      const int stride = nthr * 4;
-      const int sq = stride / D, sr = stride - (stride / D) * D;
-      for (int64_t v = tid; v < nv; v += nthr) {
-        float vals[4];
-        int r = row, ff = f;
-        bool any_live = false;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool lv = row_live(r);
-          any_live |= lv;
-          vals[k] = lv ? value(r, ff) : 0.0f;
-          if (++ff == D) {
-            ff = 0;
-            ++r;
-          }
-        }
-        if (any_live) __stcs(out4 + v, make_float4(vals[0], vals[1], vals[2], vals[3]));
-        row += sq;
-        f += sr;
-        if (f >= D) {
-          f -= D;
-          ++row;
-        }
-      }
-    } else {
-      int row = tid / D;
-      int f = tid - row * D;
-      const int sq = nthr / D, sr = nthr - (nthr / D) * D;
-      for (int64_t i = tid; i < n; i += nthr) {
-        if (row_live(row)) __stcs(out + i, value(row, f));
-        row += sq;
-        f += sr;
-        if (f >= D) {
-          f -= D;
-          ++row;
-        }
+    auto row_live = [&](int row) -> bool { return single || scal[row / A].live != 0; };
+    int row = tid / D;
+    int f = tid - row * D;
+    const int sq = nthr / D, sr = nthr - (nthr / D) * D;
+    for (int64_t i = tid; i < n; i += nthr) {
+      if (row_live(row)) __stcs(cta_out + i, value(row, f));
+      row += sq;
+      f += sr;
+      if (f >= D) {
+        f -= D;
+        ++row;
       }
     }
   }
@@ -757,7 +940,7 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     if (lt == 0 && mode != kModeReinit) {
       g.step_count[e] = sc.step_count;
       g.done[e] = static_cast<uint8_t>(sc.done);
-      if (sc.did_reset && L.episode != nullptr) L.episode[e] = sc.episode;
+      if (place && L.episode != nullptr) L.episode[e] = episode;
     }
   }
 }
@@ -862,10 +1045,45 @@ __global__ void stats_reduce_kernel(const double* __restrict__ env_stats, int64_
   }
 }
 
-template <bool CONT, bool PARTIAL, bool GRID, int MAXK>
+// Shell table for the lattice K-NN (constant memory, once per device).
+cudaError_t ensure_shell_table() {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (dev < 64 && done[dev]) return cudaSuccess;
+  int16_t off[kMaxShellOffsets];
+  int16_t begin[kMaxShells + 1];
+  int16_t d2v[kMaxShells];
+  int n = 0, ns = 0;
+  for (int d2 = 0; d2 <= kShellR2; ++d2) {
+    const int start = n;
+    for (int dy = -kShellR; dy <= kShellR; ++dy)
+      for (int dx = -kShellR; dx <= kShellR; ++dx)
+        if (dx * dx + dy * dy == d2) off[n++] = static_cast<int16_t>((dx + 64) | ((dy + 64) << 8));
+    if (n > start) {
+      begin[ns] = static_cast<int16_t>(start);
+      d2v[ns] = static_cast<int16_t>(d2);
+      ++ns;
+    }
+  }
+  begin[ns] = static_cast<int16_t>(n);
+  if ((err = cudaMemcpyToSymbol(c_shell_off, off, sizeof(int16_t) * n)) != cudaSuccess) return err;
+  if ((err = cudaMemcpyToSymbol(c_shell_begin, begin, sizeof(int16_t) * (ns + 1))) != cudaSuccess) return err;
+  if ((err = cudaMemcpyToSymbol(c_shell_d2, d2v, sizeof(int16_t) * ns)) != cudaSuccess) return err;
+  if ((err = cudaMemcpyToSymbol(c_num_shells, &ns, sizeof(int32_t))) != cudaSuccess) return err;
+  if (dev < 64) done[dev] = true;
+  return cudaSuccess;
+}
+
+template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT>
 cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                            cudaStream_t st) {
-  auto kern = tag_env_kernel<CONT, PARTIAL, GRID, MAXK>;
+  auto kern = tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT>;
+  if (!CONT && GRID) {
+    cudaError_t err = ensure_shell_table();
+    if (err != cudaSuccess) return err;
+  }
   if (p.smem_bytes > 48 * 1024) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            p.smem_bytes);
@@ -879,10 +1097,11 @@ template <bool CONT, bool PARTIAL, bool GRID>
 cudaError_t launch_k(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                      cudaStream_t st) {
   if constexpr (!PARTIAL) {
-    return launch_variant<CONT, PARTIAL, GRID, 1>(p, g, L, st);
+    return launch_variant<CONT, PARTIAL, GRID, 1, true>(p, g, L, st);
   } else {
-    if (p.K <= 8) return launch_variant<CONT, PARTIAL, GRID, 8>(p, g, L, st);
-    return launch_variant<CONT, PARTIAL, GRID, 32>(p, g, L, st);
+    if (p.K == 5) return launch_variant<CONT, PARTIAL, GRID, 5, true>(p, g, L, st);
+    if (p.K <= 8) return launch_variant<CONT, PARTIAL, GRID, 8, false>(p, g, L, st);
+    return launch_variant<CONT, PARTIAL, GRID, 32, false>(p, g, L, st);
   }
 }
 
