@@ -127,7 +127,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   if (p.use_grid) {
     // One env per CTA, one thread per agent up to the CTA cap (larger A
     // loops). WDG_TPE_MAX overrides the cap (tuning experiments).
-    int cap = 1024;
+    int cap = 512;
     if (const char* env = std::getenv("WDG_TPE_MAX")) cap = std::clamp(std::atoi(env), 32, 1024) / 32 * 32;
     p.envs_per_cta = 1;
     p.threads = std::min<int32_t>(round_up(A, 32), cap);
@@ -193,6 +193,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
     p.off_cfill = take(4 * (p.ncells + 1), 4);
     p.off_items = take(2 * A, 4);
     p.off_cellof = take(2 * A, 4);
+    if (p.lattice && p.partial && p.stage_obs) p.off_cellknn = take(2 * int64_t{p.ncells} * (p.K + 1), 4);
   }
   p.env_bytes = align16(off);
   // CTA header: per-env scalars + 64 doubles of warp scratch (scan / sums).

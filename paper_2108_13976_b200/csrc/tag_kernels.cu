@@ -144,6 +144,7 @@ struct EnvSmem {
   int32_t* cfill;
   uint16_t* items;
   uint16_t* cellof;
+  uint16_t* cellknn;  // lattice: per-cell top-(K+1) lists
 };
 
 __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
@@ -163,6 +164,7 @@ __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
   s.cfill = reinterpret_cast<int32_t*>(b + p.off_cfill);
   s.items = reinterpret_cast<uint16_t*>(b + p.off_items);
   s.cellof = reinterpret_cast<uint16_t*>(b + p.off_cellof);
+  s.cellknn = reinterpret_cast<uint16_t*>(b + p.off_cellknn);
   return s;
 }
 
@@ -253,6 +255,62 @@ __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch
     s.items[slot] = static_cast<uint16_t>(a);
   }
   __syncthreads();
+  // Each cell's items in ascending agent index (the order NeighborGrid::build
+  // produces with its serial counting sort, neighbor_grid.hpp:31-43).
+  for (int c = tid; c < p.ncells; c += nthr) {
+    const int b = s.cstart[c], e = s.cstart[c + 1];
+    for (int i = b + 1; i < e; ++i) {
+      const uint16_t v = s.items[i];
+      int k = i - 1;
+      while (k >= b && s.items[k] > v) {
+        s.items[k + 1] = s.items[k];
+        --k;
+      }
+      s.items[k + 1] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// Lattice K-NN per CELL: the top-(K+1) agents by (d2, index) seen from lattice
+// point c. Shells of equal d2 are visited in increasing order and, inside a
+// shell, candidates are taken in increasing index by repeated minimum over the
+// shell's (index-sorted) cells — no insertion network. An agent's K nearest
+// are this list minus itself. Returns the count found (< kk only if the
+// precomputed disk is exhausted; the caller then falls back per agent).
+__device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t* out, int kk) {
+  const int g = p.gc;
+  const int cy = c / g, cx = c - cy * g;
+  const int ns = c_num_shells;
+  int found = 0;
+  for (int sh = 0; sh < ns && found < kk; ++sh) {
+    const int ob = c_shell_begin[sh], oe = c_shell_begin[sh + 1];
+    int last = -1;
+    while (found < kk) {
+      int best = 0x7fffffff;
+      for (int o = ob; o < oe; ++o) {
+        const int packed = c_shell_off[o];
+        const int gx = cx + (packed & 0xff) - 64;
+        const int gy = cy + ((packed >> 8) & 0xff) - 64;
+        if (static_cast<unsigned>(gx) >= static_cast<unsigned>(g) ||
+            static_cast<unsigned>(gy) >= static_cast<unsigned>(g))
+          continue;
+        const int c2 = gy * g + gx;
+        const int e = s.cstart[c2 + 1];
+        for (int t = s.cstart[c2]; t < e; ++t) {
+          const int j = s.items[t];
+          if (j > last) {
+            best = j < best ? j : best;
+            break;
+          }
+        }
+      }
+      if (best == 0x7fffffff) break;
+      out[found++] = static_cast<uint16_t>(best);
+      last = best;
+    }
+  }
+  return found;
 }
 
 // ---- exact top-K under the (d2, index) total order ------------------------
@@ -437,10 +495,15 @@ __device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn) {
     return best;
   }
   if (exact_cell) {
+    // cells are index-sorted: the first tagger at the runner's position is
+    // the lowest-index one (tag_env.cpp:430-434)
     const int c = s.cellof[rn];
     const int e = s.cstart[c + 1];
-    for (int t = s.cstart[c]; t < e; ++t) consider(s.items[t]);
-    return best;
+    for (int t = s.cstart[c]; t < e; ++t) {
+      const int j = s.items[t];
+      if (s.tag[j] && s.x[j] == rx && s.y[j] == ry) return j;
+    }
+    return -1;
   }
   const float R = __fadd_rn(__fmul_rn(radius, 1.001f), 1e-6f);
   const int x0 = cell_coord<CONT>(__fsub_rn(rx, R), p), x1 = cell_coord<CONT>(__fadd_rn(rx, R), p);
@@ -829,7 +892,7 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     build_grid<CONT>(s, p, scratch);
   }
   __syncthreads();
-  const bool lattice_ok = !CONT && GRID && scal[0].lattice_ok;
+  const bool lattice_ok = !CONT && GRID && p.lattice && scal[0].lattice_ok;
 
   // Phase 7: K-NN + observation rows (write_obs_row, tag_env.cpp:165-212).
   const int64_t cta_env0 = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
@@ -841,12 +904,28 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     // warp then streams the contiguous block of its rows with 16-byte stores.
     float* stage = reinterpret_cast<float*>(smem + p.off_stage) + warp * p.stage_floats;
     const bool vec = ((static_cast<int64_t>(p.envs_per_cta) * A * D) & 3) == 0;
+    const bool cell_lists = PARTIAL && lattice_ok;  // GRID => single env per CTA
+    const int kk = p.K + 1;
+    if (cell_lists) {
+      for (int c = tid; c < p.ncells; c += blockDim.x) {
+        s.cfill[c] = s.cstart[c + 1] > s.cstart[c] ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
+      }
+      __syncthreads();
+    }
     for (int base = 0; base < A; base += tpe) {
       const int a = base + lt;
       const bool valid = live && a < A;
       if (valid) {
         float* row = stage + lane * D;
-        if (PARTIAL && s.act[a]) {
+        const int cl = cell_lists ? s.cellof[a] : 0;
+        if (cell_lists && s.act[a] && s.cfill[cl] == kk) {
+          const uint16_t* lst = s.cellknn + cl * kk;
+          int self_pos = kk;
+          for (int t = 0; t < kk; ++t)
+            if (lst[t] == a) self_pos = t;
+          write_row<CONT>(s, p, sc.step_count, a, row,
+                          [&](int n) { return static_cast<int>(lst[n + (n >= self_pos ? 1 : 0)]); });
+        } else if (PARTIAL && s.act[a]) {
           TopK<MAXK, EXACT> top;
           knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top);
           write_row<CONT>(s, p, sc.step_count, a, row, [&](int n) {

@@ -76,9 +76,9 @@ def main():
         if want not in kname:
             continue
         # match function by template args
-        targs = re.findall(r"\((?:bool|int)\)(\w+)", kname)
+        targs = re.findall(r"\((bool|int)\)(\w+)", kname)
         mangled = [f for f in funcs if "tag_env_kernel" in f]
-        sig = "".join(("Lb1E" if a == "1" else "Lb0E") if i < 3 else f"Li{a}E" for i, a in enumerate(targs))
+        sig = "".join((f"Lb{a}E" if t == "bool" else f"Li{a}E") for t, a in targs)
         cand = [f for f in mangled if sig in f.replace("ILb", "Lb")] or mangled
         table = funcs[cand[0]]
         agg = defaultdict(lambda: [0, 0, 0])
