@@ -190,9 +190,10 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     W.lib().wdg_set_device(local_rank)
     stream = torch.cuda.current_stream()
-    E = ENVS_PER_GPU
+    from paper_2108_13976_b200.sharding import weak_shard
+    env_offset, E = weak_shard(ENVS_PER_GPU, rank)
     cfg = W.TagConfig(**C2)
-    ws = W.Workspace(cfg, E, env_offset=rank * E, stream=stream)
+    ws = W.Workspace(cfg, E, env_offset=env_offset, stream=stream)
     drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, cfg.seed)
     A, Cc, V, D = cfg.num_agents(), cfg.action_categories(), cfg.action_choices(), cfg.obs_dim()
     geo = ws.plan.geometry()

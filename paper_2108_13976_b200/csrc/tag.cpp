@@ -127,7 +127,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   if (p.use_grid) {
     // One env per CTA, one thread per agent up to the CTA cap (larger A
     // loops). WDG_TPE_MAX overrides the cap (tuning experiments).
-    int cap = 512;
+    int cap = 256;  // 4 CTAs (envs) per SM overlap each other's barriers (measured best)
     if (const char* env = std::getenv("WDG_TPE_MAX")) cap = std::clamp(std::atoi(env), 32, 1024) / 32 * 32;
     p.envs_per_cta = 1;
     p.threads = std::min<int32_t>(round_up(A, 32), cap);

@@ -1,0 +1,34 @@
+// Compile-checked example of the reference-side C++ integration through
+// include/warp_b200.hpp (tests/test_abi.py builds and links it; runs it on a
+// GPU in tests/test_parity_gpu.py::test_cpp_facade_example).
+#include <cstdio>
+
+#include "warp_b200.hpp"
+
+int main() {
+  using namespace warp_b200;
+  TagConfig cfg;
+  cfg.num_taggers = 20;
+  cfg.num_runners = 80;
+  cfg.obs_mode = WDG_OBS_PARTIAL;
+  cfg.grid_size = 10;
+  cfg.episode_length = 25;
+  try {
+    DataStore store(16, cfg.num_agents());           // build_workspace (harness.cpp:402-423)
+    register_tag_arrays(store, cfg);
+    store.lock();
+    TagPlan plan(store, cfg);
+    ResetManager resets(store, true, tag_zero_on_reset(), &plan);
+    RolloutDriver driver(store, plan, &resets, cfg.seed);
+    driver.run(40);                                  // RolloutDriver::run (harness.cpp:492-494)
+    driver.check_errors();
+    const std::vector<double> st = driver.stats();
+    const std::vector<float> obs = store.pull<float>(kObservations, 0, 1);
+    std::printf("episodes=%.0f tag_events=%.0f env_steps=%.0f obs[0]=%g\n", st[WDG_STAT_EPISODES],
+                st[WDG_STAT_TAG_EVENTS], st[WDG_STAT_ENV_STEPS], obs[0]);
+    return st[WDG_STAT_ENV_STEPS] == 16 * 40 ? 0 : 1;
+  } catch (const Error& e) {
+    std::fprintf(stderr, "error %d: %s\n", static_cast<int>(e.code()), e.what());
+    return 2;
+  }
+}

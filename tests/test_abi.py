@@ -105,3 +105,22 @@ def test_no_gpu_fails_loudly():
         W.DataStore(2, 5)
     assert ei.value.code == W.CUDA_ERROR
     assert "no CPU fallback" in str(ei.value)
+
+
+def build_cpp_example(tmp_dir):
+    """Builds tests/cpp/facade_example.cpp against include/warp_b200.hpp and
+    the product library (what a reference-side C++ integration compiles)."""
+    lib_dir = os.path.dirname(W.library_path())
+    exe = os.path.join(str(tmp_dir), "facade_example")
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "facade_example.cpp"), "-L", lib_dir, "-lwdg_b200",
+                    f"-Wl,-rpath,{lib_dir}", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_facade_builds_and_fails_loudly_without_gpu(tmp_path):
+    exe = build_cpp_example(tmp_path)
+    if W.device_count() > 0:
+        pytest.skip("GPU present: the run is covered by test_parity_gpu")
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 2 and "no CUDA device" in r.stderr

@@ -455,3 +455,14 @@ def test_unsupported_shapes_fail_loudly():
         dc, _ = cfg_pair(num_taggers=10, num_runners=40, obs_mode=O.PARTIAL, k_nearest=40)
         W.Workspace(dc, 2)
     assert ei.value.code == W.INVALID_CONFIG
+
+
+def test_cpp_facade_example(tmp_path):
+    """The header-only C++ facade (include/warp_b200.hpp) drives the same
+    fused rollout from C++ (reference-side integration path)."""
+    import subprocess
+    from test_abi import build_cpp_example
+    exe = build_cpp_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "env_steps=640" in r.stdout

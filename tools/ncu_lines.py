@@ -16,7 +16,7 @@ import tempfile
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SO = os.path.join(ROOT, "paper_2108_13976_b200", "lib", "libwdg_b200.so")
+SO = os.environ.get("WDG_SO", os.path.join(ROOT, "paper_2108_13976_b200", "lib", "libwdg_b200.so"))
 
 
 def sass_metrics(rep):
@@ -42,7 +42,7 @@ def sass_metrics(rep):
 
 def line_table():
     d = tempfile.mkdtemp()
-    subprocess.run(["cuobjdump", "-xelf", "all", SO], cwd=d, capture_output=True)
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(SO)], cwd=d, capture_output=True)
     cub = [f for f in os.listdir(d) if f.startswith("tag_kernels")][0]
     txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True,
                          text=True).stdout
