@@ -129,6 +129,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
     // loops). WDG_TPE_MAX overrides the cap (tuning experiments).
     int cap = 256;  // 4 CTAs (envs) per SM overlap each other's barriers (measured best)
     if (const char* env = std::getenv("WDG_TPE_MAX")) cap = std::clamp(std::atoi(env), 32, 1024) / 32 * 32;
+    cap = std::min(cap, kMaxThreadsPerCta);
     p.envs_per_cta = 1;
     p.threads = std::min<int32_t>(round_up(A, 32), cap);
     p.threads_per_env = p.threads;
@@ -136,7 +137,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
     // Smallest CTA (in warps) that holds >= 1 env, grown while the grid keeps
     // >= 2 CTAs per SM so small-A sweeps spread over all 148 SMs.
     int w = static_cast<int>((A + 31) / 32);
-    for (int cand = w; cand <= 8; cand *= 2) {
+    for (int cand = w; cand <= std::min(8, kMaxThreadsPerCta / 32); cand *= 2) {
       const int64_t epc = (32 * cand) / A;
       const int64_t ctas = (store.num_envs() + epc - 1) / epc;
       if (cand == w || ctas >= 2 * kNumSMs) w = cand;
@@ -176,17 +177,17 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
     return at;
   };
   take(4 * A, 16);  // x at 0
-  p.off_y = take(4 * A, 4);
+  p.off_y = take(4 * A, 16);
   if (p.continuous) {
-    p.off_speed = take(4 * A, 4);
-    p.off_dir = take(4 * A, 4);
-    p.off_sin = take(4 * A, 4);
-    p.off_cos = take(4 * A, 4);
+    p.off_speed = take(4 * A, 16);
+    p.off_dir = take(4 * A, 16);
+    p.off_sin = take(4 * A, 16);
+    p.off_cos = take(4 * A, 16);
   }
-  p.off_cred = take(4 * A, 4);
-  p.off_tag = take(A, 1);
-  p.off_act = take(A, 1);
-  p.off_tagged = take(A, 1);
+  p.off_cred = take(4 * A, 16);
+  p.off_tag = take(A, 16);
+  p.off_act = take(A, 16);
+  p.off_tagged = take(A, 16);
   if (p.partial && !p.stage_obs) p.off_knn = take(2 * A * p.K, 4);
   if (p.use_grid) {
     p.off_cstart = take(4 * (p.ncells + 1), 4);

@@ -33,6 +33,10 @@
 namespace wdg {
 namespace {
 
+#ifndef WDG_SAMPLE_UNROLL
+#define WDG_SAMPLE_UNROLL 2
+#endif
+constexpr int kSampleUnroll = WDG_SAMPLE_UNROLL;  // agents sampled in flight per thread
 constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
 constexpr float kTwoPiF = 6.28318530717958647692f;  // tag_env.hpp:84
 
@@ -285,6 +289,47 @@ __device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t
   int found = 0;
   for (int sh = 0; sh < ns && found < kk; ++sh) {
     const int ob = c_shell_begin[sh], oe = c_shell_begin[sh + 1];
+    if (oe - ob <= 8) {
+      // k-way merge with one cursor per cell of the shell (registers).
+      int cur[8], end[8], head[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        cur[q] = 0;
+        end[q] = 0;
+        if (q < oe - ob) {
+          const int packed = c_shell_off[ob + q];
+          const int gx = cx + (packed & 0xff) - 64;
+          const int gy = cy + ((packed >> 8) & 0xff) - 64;
+          if (static_cast<unsigned>(gx) < static_cast<unsigned>(g) &&
+              static_cast<unsigned>(gy) < static_cast<unsigned>(g)) {
+            const int c2 = gy * g + gx;
+            cur[q] = s.cstart[c2];
+            end[q] = s.cstart[c2 + 1];
+          }
+        }
+        head[q] = cur[q] < end[q] ? static_cast<int>(s.items[cur[q]]) : 0x7fffffff;
+      }
+      while (found < kk) {
+        int best = head[0], bq = 0;
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+          if (head[q] < best) {
+            best = head[q];
+            bq = q;
+          }
+        }
+        if (best == 0x7fffffff) break;
+        out[found++] = static_cast<uint16_t>(best);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q == bq) {
+            ++cur[q];
+            head[q] = cur[q] < end[q] ? static_cast<int>(s.items[cur[q]]) : 0x7fffffff;
+          }
+        }
+      }
+      continue;
+    }
     int last = -1;
     while (found < kk) {
       int best = 0x7fffffff;
@@ -558,42 +603,64 @@ __device__ __forceinline__ float obs_value(const EnvSmem& s, const TagDevConfig&
 // Writes one agent's full observation row (write_obs_row) to `out`
 // (a warp staging buffer in shared memory). `nb(n)` yields the n-th visible
 // neighbour.
-template <bool CONT, class NB>
+template <bool CONT, int VIS_CT, class NB>
 __device__ __forceinline__ void write_row(const EnvSmem& s, const TagDevConfig& p, int32_t step_count,
                                           int a, float* out, NB nb) {
+  // VIS_CT > 0: visible count known at compile time (partial obs, exact K)
+  constexpr int NBF = CONT ? 7 : 4;
+  constexpr int D_CT = VIS_CT * NBF + (CONT ? 5 : 2) + 1;
+  const int vis = VIS_CT > 0 ? VIS_CT : p.vis;
+  const int D = VIS_CT > 0 ? D_CT : p.D;
   if (!s.act[a]) {
-    for (int f = 0; f < p.D; ++f) out[f] = 0.0f;
+#pragma unroll
+    for (int f = 0; f < (VIS_CT > 0 ? D_CT : 1); ++f) out[f] = 0.0f;
+    if (VIS_CT == 0)
+      for (int f = 1; f < D; ++f) out[f] = 0.0f;
     return;
   }
   const float sx = s.x[a], sy = s.y[a];
   const float iw = p.inv_world;
-  int o = 0;
-  for (int n = 0; n < p.vis; ++n) {
+#pragma unroll
+  for (int n = 0; n < (VIS_CT > 0 ? VIS_CT : 1); ++n) {
+    if (VIS_CT == 0 && n >= vis) break;
     const int j = nb(n);
-    out[o + 0] = __fmul_rn(__fsub_rn(s.x[j], sx), iw);
-    out[o + 1] = __fmul_rn(__fsub_rn(s.y[j], sy), iw);
-    out[o + 2] = s.tag[j] ? 1.0f : 0.0f;
-    out[o + 3] = s.act[j] ? 1.0f : 0.0f;
+    float* o = out + n * NBF;
+    o[0] = __fmul_rn(__fsub_rn(s.x[j], sx), iw);
+    o[1] = __fmul_rn(__fsub_rn(s.y[j], sy), iw);
+    o[2] = s.tag[j] ? 1.0f : 0.0f;
+    o[3] = s.act[j] ? 1.0f : 0.0f;
     if (CONT) {
-      out[o + 4] = __fmul_rn(s.sp[j], inv_ms(p, j));
-      out[o + 5] = s.sn[j];
-      out[o + 6] = s.cs[j];
-      o += 7;
-    } else {
-      o += 4;
+      o[4] = __fmul_rn(s.sp[j], inv_ms(p, j));
+      o[5] = s.sn[j];
+      o[6] = s.cs[j];
     }
   }
-  out[o + 0] = __fmul_rn(sx, iw);
-  out[o + 1] = __fmul_rn(sy, iw);
-  if (CONT) {
-    out[o + 2] = __fmul_rn(s.sp[a], inv_ms(p, a));
-    out[o + 3] = s.sn[a];
-    out[o + 4] = s.cs[a];
-    o += 5;
-  } else {
-    o += 2;
+  if (VIS_CT == 0) {
+    for (int n = 1; n < vis; ++n) {
+      const int j = nb(n);
+      float* o = out + n * NBF;
+      o[0] = __fmul_rn(__fsub_rn(s.x[j], sx), iw);
+      o[1] = __fmul_rn(__fsub_rn(s.y[j], sy), iw);
+      o[2] = s.tag[j] ? 1.0f : 0.0f;
+      o[3] = s.act[j] ? 1.0f : 0.0f;
+      if (CONT) {
+        o[4] = __fmul_rn(s.sp[j], inv_ms(p, j));
+        o[5] = s.sn[j];
+        o[6] = s.cs[j];
+      }
+    }
   }
-  out[o] = __fmul_rn(static_cast<float>(step_count), p.inv_episode);
+  float* o = out + vis * NBF;
+  o[0] = __fmul_rn(sx, iw);
+  o[1] = __fmul_rn(sy, iw);
+  if (CONT) {
+    o[2] = __fmul_rn(s.sp[a], inv_ms(p, a));
+    o[3] = s.sn[a];
+    o[4] = s.cs[a];
+    o[5] = __fmul_rn(static_cast<float>(step_count), p.inv_episode);
+  } else {
+    o[2] = __fmul_rn(static_cast<float>(step_count), p.inv_episode);
+  }
 }
 
 // sinf/cosf evaluated in f64 and rounded once: the correctly-rounded value
@@ -608,12 +675,94 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// apply_move for one agent held in shared memory (tag_env.cpp:148-160,
+// move_discrete / move_continuous tag_env.hpp:71-100). Inactive agents stay.
+template <bool CONT>
+__device__ __forceinline__ void move_agent(const EnvSmem& s, const TagDevConfig& p, int a, int act0,
+                                           int act1) {
+  if (!s.act[a]) return;
+  if (!CONT) {
+    float x = s.x[a], y = s.y[a];
+    switch (act0) {
+      case 1: y = __fadd_rn(y, 1.0f); break;
+      case 2: y = __fsub_rn(y, 1.0f); break;
+      case 3: x = __fsub_rn(x, 1.0f); break;
+      case 4: x = __fadd_rn(x, 1.0f); break;
+      default: break;
+    }
+    s.x[a] = min_ref(max_ref(x, 0.0f), p.world_hi);
+    s.y[a] = min_ref(max_ref(y, 0.0f), p.world_hi);
+  } else {
+    float dir = s.dir[a], sp = s.sp[a];
+    if (act1 == 0) dir = __fsub_rn(dir, p.turn_delta);
+    if (act1 == 2) dir = __fadd_rn(dir, p.turn_delta);
+    while (dir >= kTwoPiF) dir = __fsub_rn(dir, kTwoPiF);
+    while (dir < 0.0f) dir = __fadd_rn(dir, kTwoPiF);
+    if (act0 == 0) sp = __fsub_rn(sp, p.accel_delta);
+    if (act0 == 2) sp = __fadd_rn(sp, p.accel_delta);
+    const float ms = a < p.T ? p.max_speed_tagger : p.max_speed_runner;
+    sp = min_ref(max_ref(sp, 0.0f), ms);
+    const float x = __fadd_rn(s.x[a], __fmul_rn(sp, cos_ref(dir)));
+    const float y = __fadd_rn(s.y[a], __fmul_rn(sp, sin_ref(dir)));
+    s.x[a] = min_ref(max_ref(x, 0.0f), p.world_hi);
+    s.y[a] = min_ref(max_ref(y, 0.0f), p.world_hi);
+    s.dir[a] = dir;
+    s.sp[a] = sp;
+  }
+}
+
+// Five f64 logits of one discrete row with 16-byte loads where aligned
+// (rows are 40 B apart: even rows start 16-B aligned, odd rows 8-B).
+__device__ __forceinline__ void load_row5(const double* __restrict__ z, int64_t row, double* out) {
+  const double* r = z + row * 5;
+  if ((row & 1) == 0) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(r));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(r + 2));
+    out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y; out[4] = __ldg(r + 4);
+  } else {
+    out[0] = __ldg(r);
+    const double2 a = __ldg(reinterpret_cast<const double2*>(r + 1));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(r + 3));
+    out[1] = a.x; out[2] = a.y; out[3] = b.x; out[4] = b.y;
+  }
+}
+
+// sample_from_logits (sampler.hpp:18-30) on a register row of 5.
+__device__ __forceinline__ int32_t sample5(const double* z, double u, bool& nonfinite) {
+  double zmax = z[0];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    nonfinite |= !isfinite(z[i]);
+    zmax = zmax < z[i] ? z[i] : zmax;
+  }
+  double ev[5];
+  double total = 0.0;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    ev[i] = exp(z[i] - zmax);
+    total = __dadd_rn(total, ev[i]);
+  }
+  const double target = __dmul_rn(u, total);
+  double cum = 0.0;
+  int32_t pick = 4;
+  bool found = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    cum = __dadd_rn(cum, ev[i]);
+    if (!found && target < cum) {
+      pick = i;
+      found = true;
+    }
+  }
+  return pick;
+}
+
 // ---- the env-step kernel --------------------------------------------------
 // Thread layout: tid = le * tpe + lt (le = env slot in the CTA, lt = lane in
 // the env). Per-agent loops run over `base` in warp-uniform steps so warp
 // collectives are legal; agent a = base + lt.
 template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT>
-__global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, const TagDevArrays g,
+__global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_kernel(const TagDevConfig p, const TagDevArrays g,
                                                        const TagLaunch L) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x;
@@ -642,10 +791,39 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
   EnvScalars& sc = scal[env_ok ? le : 0];
   const int64_t ga = e * A;
 
+  // Single-env CTAs with A % 4 == 0 move 4 consecutive agents per thread in
+  // the per-agent phases so every global access is a 16-byte (or 4-byte for
+  // flags) vector and the logits rows of a thread are contiguous.
+  const bool vec4 = GRID && (A & 3) == 0;
+
   // Phase 0: stage the env's agent state in shared memory.
   bool integral = true;
+  if (live && vec4) {
+    for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
+      if (mode != kModeReinit) {
+        const float4 x4 = *reinterpret_cast<const float4*>(g.loc_x + ga + a0);
+        const float4 y4 = *reinterpret_cast<const float4*>(g.loc_y + ga + a0);
+        *reinterpret_cast<float4*>(s.x + a0) = x4;
+        *reinterpret_cast<float4*>(s.y + a0) = y4;
+        const float xs[4] = {x4.x, x4.y, x4.z, x4.w}, ys[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          integral &= (xs[k] == truncf(xs[k])) && (ys[k] == truncf(ys[k])) && xs[k] >= 0.0f &&
+                      ys[k] >= 0.0f && xs[k] <= p.world_hi && ys[k] <= p.world_hi;
+        }
+        *reinterpret_cast<uint32_t*>(s.act + a0) = *reinterpret_cast<const uint32_t*>(g.active + ga + a0);
+        if (CONT) {
+          *reinterpret_cast<float4*>(s.sp + a0) = *reinterpret_cast<const float4*>(g.speed + ga + a0);
+          *reinterpret_cast<float4*>(s.dir + a0) = *reinterpret_cast<const float4*>(g.direction + ga + a0);
+        }
+      }
+      *reinterpret_cast<uint32_t*>(s.tag + a0) = *reinterpret_cast<const uint32_t*>(g.is_tagger + ga + a0);
+      *reinterpret_cast<int4*>(s.cred + a0) = make_int4(0, 0, 0, 0);
+      *reinterpret_cast<uint32_t*>(s.tagged + a0) = 0u;
+    }
+  }
   if (live) {
-    for (int a = lt; a < A; a += tpe) {
+    for (int a = vec4 ? A : lt; a < A; a += tpe) {
       if (mode != kModeReinit) {
         const float x = g.loc_x[ga + a], y = g.loc_y[ga + a];
         s.x[a] = x;
@@ -685,7 +863,49 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     if (live) {
       const uint64_t h_env = absorb(L.action_h_step, static_cast<uint64_t>(p.env_offset + e));
       bool nonfinite = false;
-      for (int a = lt; a < A; a += tpe) {
+      if (vec4) {
+        for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
+          int32_t act0[4], act1[4] = {1, 1, 1, 1};
+          if (mode == kModeFused) {
+#pragma unroll kSampleUnroll
+            for (int k = 0; k < 4; ++k) {
+              const int a = a0 + k;
+              const int64_t row = (ga + a) * p.C;
+              const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
+              const double u0 = to_unit(absorb(absorb(h_ag, 0), 0));
+              if (!CONT && p.V == 5) {
+                double z[5];
+                load_row5(L.logits, row, z);
+                act0[k] = sample5(z, u0, nonfinite);
+              } else {
+                act0[k] = sample_row(L.logits + row * p.V, p.V, u0, nonfinite);
+              }
+              if (CONT) {
+                const double u1 = to_unit(absorb(absorb(h_ag, 1), 0));
+                act1[k] = sample_row(L.logits + (row + 1) * p.V, p.V, u1, nonfinite);
+              }
+            }
+            if (CONT) {
+              int4* dst = reinterpret_cast<int4*>(g.actions + (ga + a0) * 2);
+              dst[0] = make_int4(act0[0], act1[0], act0[1], act1[1]);
+              dst[1] = make_int4(act0[2], act1[2], act0[3], act1[3]);
+            } else {
+              *reinterpret_cast<int4*>(g.actions + ga + a0) = make_int4(act0[0], act0[1], act0[2], act0[3]);
+            }
+          } else if (CONT) {
+            const int4* src = reinterpret_cast<const int4*>(g.actions + (ga + a0) * 2);
+            const int4 v0 = src[0], v1 = src[1];
+            act0[0] = v0.x; act1[0] = v0.y; act0[1] = v0.z; act1[1] = v0.w;
+            act0[2] = v1.x; act1[2] = v1.y; act0[3] = v1.z; act1[3] = v1.w;
+          } else {
+            const int4 v = *reinterpret_cast<const int4*>(g.actions + ga + a0);
+            act0[0] = v.x; act0[1] = v.y; act0[2] = v.z; act0[3] = v.w;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) move_agent<CONT>(s, p, a0 + k, act0[k], act1[k]);
+        }
+      }
+      for (int a = vec4 ? A : lt; a < A; a += tpe) {
         int32_t act0, act1 = 1;
         const int64_t row = (ga + a) * p.C;
         if (mode == kModeFused) {
@@ -776,8 +996,33 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
     reset_now = live && mode == kModeFused && L.do_reset && sc.done;
     const bool track = mode == kModeFused && L.track;
     double rt = 0.0, rr = 0.0;
+    if (live && vec4) {
+      for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
+        const int4 c4 = *reinterpret_cast<const int4*>(s.cred + a0);
+        const uint32_t tg4 = *reinterpret_cast<const uint32_t*>(s.tag + a0);
+        const uint32_t td4 = *reinterpret_cast<const uint32_t*>(s.tagged + a0);
+        const int cr[4] = {c4.x, c4.y, c4.z, c4.w};
+        float r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool is_t = (tg4 >> (8 * k)) & 0xffu;
+          const bool was = (td4 >> (8 * k)) & 0xffu;
+          r[k] = is_t ? __fmul_rn(p.reward_per_tag, static_cast<float>(cr[k])) : (was ? p.penalty : 0.0f);
+          if (a0 + k < p.T) rt += static_cast<double>(r[k]); else rr += static_cast<double>(r[k]);
+        }
+        if (reset_now) {
+          *reinterpret_cast<float4*>(g.rewards + ga + a0) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<int4*>(g.credits + ga + a0) = make_int4(0, 0, 0, 0);
+          *reinterpret_cast<uint32_t*>(g.tagged + ga + a0) = 0u;
+        } else {
+          *reinterpret_cast<float4*>(g.rewards + ga + a0) = make_float4(r[0], r[1], r[2], r[3]);
+          *reinterpret_cast<int4*>(g.credits + ga + a0) = c4;
+          *reinterpret_cast<uint32_t*>(g.tagged + ga + a0) = td4;
+        }
+      }
+    }
     if (live) {
-      for (int a = lt; a < A; a += tpe) {
+      for (int a = vec4 ? A : lt; a < A; a += tpe) {
         const float r = s.tag[a] ? __fmul_rn(p.reward_per_tag, static_cast<float>(s.cred[a]))
                                  : (s.tagged[a] ? p.penalty : 0.0f);
         if (a < p.T) rt += static_cast<double>(r); else rr += static_cast<double>(r);
@@ -923,12 +1168,13 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
           int self_pos = kk;
           for (int t = 0; t < kk; ++t)
             if (lst[t] == a) self_pos = t;
-          write_row<CONT>(s, p, sc.step_count, a, row,
-                          [&](int n) { return static_cast<int>(lst[n + (n >= self_pos ? 1 : 0)]); });
+          write_row<CONT, (EXACT ? MAXK : 0)>(
+              s, p, sc.step_count, a, row,
+              [&](int n) { return static_cast<int>(lst[n + (n >= self_pos ? 1 : 0)]); });
         } else if (PARTIAL && s.act[a]) {
           TopK<MAXK, EXACT> top;
           knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top);
-          write_row<CONT>(s, p, sc.step_count, a, row, [&](int n) {
+          write_row<CONT, (EXACT ? MAXK : 0)>(s, p, sc.step_count, a, row, [&](int n) {
             int j = top.i[0];
 #pragma unroll
             for (int t = 1; t < MAXK; ++t)
@@ -936,7 +1182,7 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
             return j;
           });
         } else {
-          write_row<CONT>(s, p, sc.step_count, a, row, [&](int n) { return n < a ? n : n + 1; });
+          write_row<CONT, 0>(s, p, sc.step_count, a, row, [&](int n) { return n < a ? n : n + 1; });
         }
       }
       __syncwarp();
@@ -1006,8 +1252,19 @@ __global__ void __launch_bounds__(1024) tag_env_kernel(const TagDevConfig p, con
   }
 
   // Phase 8: write back the env's state.
+  if (live && vec4) {
+    for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
+      *reinterpret_cast<float4*>(g.loc_x + ga + a0) = *reinterpret_cast<const float4*>(s.x + a0);
+      *reinterpret_cast<float4*>(g.loc_y + ga + a0) = *reinterpret_cast<const float4*>(s.y + a0);
+      *reinterpret_cast<uint32_t*>(g.active + ga + a0) = *reinterpret_cast<const uint32_t*>(s.act + a0);
+      if (CONT) {
+        *reinterpret_cast<float4*>(g.speed + ga + a0) = *reinterpret_cast<const float4*>(s.sp + a0);
+        *reinterpret_cast<float4*>(g.direction + ga + a0) = *reinterpret_cast<const float4*>(s.dir + a0);
+      }
+    }
+  }
   if (live) {
-    for (int a = lt; a < A; a += tpe) {
+    for (int a = vec4 ? A : lt; a < A; a += tpe) {
       g.loc_x[ga + a] = s.x[a];
       g.loc_y[ga + a] = s.y[a];
       g.active[ga + a] = s.act[a];

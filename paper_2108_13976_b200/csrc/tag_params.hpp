@@ -7,6 +7,18 @@
 
 namespace wdg {
 
+// Compile-time CTA shape limits of the env kernel: max threads per CTA and
+// the minimum resident CTAs per SM given to __launch_bounds__ (register cap =
+// 65536 / (threads * blocks)). Overridable for tuning builds.
+#ifndef WDG_MAX_THREADS
+#define WDG_MAX_THREADS 256
+#endif
+#ifndef WDG_MIN_BLOCKS
+#define WDG_MIN_BLOCKS 4
+#endif
+inline constexpr int kMaxThreadsPerCta = WDG_MAX_THREADS;
+inline constexpr int kMinBlocksPerSm = WDG_MIN_BLOCKS;
+
 // Kernel modes (one kernel body, phase set chosen per launch; uniform per CTA).
 enum TagMode : int32_t {
   kModeStep = 0,    // StepEngine::run_step: move -> resolve -> observe+reward
