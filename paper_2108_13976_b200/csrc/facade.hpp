@@ -234,7 +234,16 @@ class Rollout {
   cudaStream_t copy_ = nullptr;
   double* dlog_[2] = {nullptr, nullptr};
   cudaEvent_t h2d_done_[2] = {nullptr, nullptr};
-  cudaEvent_t kern_done_[2] = {nullptr, nullptr};  // mix64(substream(seed, kStreamActions))
+  cudaEvent_t kern_done_[2] = {nullptr, nullptr};
+  // CUDA-graph replay of kGraphSteps fused launches (run()).
+  void build_graph();
+  void drop_graph();
+  static constexpr int kGraphSteps = 16;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int64_t* step_dev_ = nullptr;
+  const double* graph_logits_ = nullptr;
+  float graph_bias_ = 0.0f;
+  cudaStream_t graph_stream_ = nullptr;  // mix64(substream(seed, kStreamActions))
 };
 
 // Host-side RNG prefix helpers (rng.hpp:23-53).

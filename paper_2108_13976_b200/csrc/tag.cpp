@@ -509,6 +509,8 @@ Rollout::Rollout(DataStore& store, TagPlan& plan, ResetManager* resets, uint64_t
 }
 
 Rollout::~Rollout() {
+  drop_graph();
+  if (step_dev_) cudaFree(step_dev_);
   for (int i = 0; i < 2; ++i) {
     if (dlog_[i]) cudaFree(dlog_[i]);
     if (h2d_done_[i]) cudaEventDestroy(h2d_done_[i]);
@@ -627,8 +629,61 @@ void Rollout::reduce_stats_into(double* device_out) {
   cuda_check(launch_stats_reduce(env_stats_, plan_.dev().E, device_out, store_.stream()), "stats reduce");
 }
 
+void Rollout::drop_graph() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  graph_exec_ = nullptr;
+}
+
+// Captures kGraphSteps fused launches whose step index is read on device as
+// *step_dev_ + i, so one instantiated graph replays any window of steps.
+void Rollout::build_graph() {
+  drop_graph();
+  if (step_dev_ == nullptr) cuda_check(cudaMalloc(&step_dev_, sizeof(int64_t)), "cudaMalloc(step)");
+  cudaStream_t st = store_.stream();
+  cudaStream_t cap = st;
+  bool own = false;
+  if (cap == nullptr) {  // the legacy default stream cannot be captured
+    cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
+    own = true;
+  }
+  cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+  cudaError_t err = cudaSuccess;
+  for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
+    TagLaunch L = fused_launch(0);
+    L.step_dev = step_dev_;
+    L.step_add = i;
+    L.action_h0 = h_actions0_;
+    TagDevConfig d = plan_.dev();
+    d.fault_bias = fault_tag_radius_bias();
+    err = launch_tag_kernel(d, bind_dev_arrays(store_, plan_.config()), L, cap);
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t end = cudaStreamEndCapture(cap, &graph);
+  if (own) cudaStreamDestroy(cap);
+  cuda_check(err, "graph capture launch");
+  cuda_check(end, "end capture");
+  err = cudaGraphInstantiate(&graph_exec_, graph, 0);
+  cudaGraphDestroy(graph);
+  cuda_check(err, "graph instantiate");
+  graph_logits_ = logits_;
+  graph_bias_ = fault_tag_radius_bias();
+  graph_stream_ = st;
+}
+
 void Rollout::run(int64_t steps) {
   if (steps < 0) raise(Errc::invalid_argument, "rollout run: steps must be >= 0");
+  if (graphs_ && fused_ok() && steps >= kGraphSteps) {
+    if (graph_exec_ == nullptr || graph_logits_ != logits_ || graph_bias_ != fault_tag_radius_bias() ||
+        graph_stream_ != store_.stream()) {
+      build_graph();
+    }
+    while (steps >= kGraphSteps) {
+      cuda_check(launch_set_counter(step_dev_, t_, store_.stream()), "set step counter");
+      cuda_check(cudaGraphLaunch(graph_exec_, store_.stream()), "graph launch");
+      t_ += kGraphSteps;
+      steps -= kGraphSteps;
+    }
+  }
   for (int64_t i = 0; i < steps; ++i) step();
 }
 

@@ -34,7 +34,7 @@ namespace wdg {
 namespace {
 
 #ifndef WDG_SAMPLE_UNROLL
-#define WDG_SAMPLE_UNROLL 2
+#define WDG_SAMPLE_UNROLL 4
 #endif
 constexpr int kSampleUnroll = WDG_SAMPLE_UNROLL;  // agents sampled in flight per thread
 constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
@@ -861,7 +861,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
   if (mode != kModeReinit) {
     // Phase 1: sample (fused) + move (apply_move, tag_env.cpp:148-160).
     if (live) {
-      const uint64_t h_env = absorb(L.action_h_step, static_cast<uint64_t>(p.env_offset + e));
+      const uint64_t h_step =
+          L.step_dev != nullptr
+              ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
+              : L.action_h_step;
+      const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
       bool nonfinite = false;
       if (vec4) {
         for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
@@ -1497,6 +1501,15 @@ cudaError_t launch_restore_zero(const ResetRowDesc* descs, int ndesc, const uint
                                 uint8_t* done, int32_t* episode, int64_t E, cudaStream_t st) {
   restore_zero_kernel<<<static_cast<unsigned>(E), 128, 0, st>>>(descs, ndesc, mask, done, episode,
                                                                 E);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void set_counter_kernel(int64_t* ptr, int64_t value) { *ptr = value; }
+}  // namespace
+
+cudaError_t launch_set_counter(int64_t* ptr, int64_t value, cudaStream_t st) {
+  set_counter_kernel<<<1, 1, 0, st>>>(ptr, value);
   return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ namespace wdg {
 #define WDG_MAX_THREADS 256
 #endif
 #ifndef WDG_MIN_BLOCKS
-#define WDG_MIN_BLOCKS 4
+#define WDG_MIN_BLOCKS 3
 #endif
 inline constexpr int kMaxThreadsPerCta = WDG_MAX_THREADS;
 inline constexpr int kMinBlocksPerSm = WDG_MIN_BLOCKS;
@@ -94,6 +94,12 @@ struct TagLaunch {
   int32_t track = 0;             // fused: EpisodeTracker stats
   int32_t init_episode = 0;      // reinit: 1 = registration (episode stays 0)
   uint64_t action_h_step = 0;    // absorb(mix64(substream(seed,kStreamActions)), step)
+  // Graph-replay mode: step = *step_dev + step_add, hashed on device from
+  // action_h0 = mix64(substream(seed, kStreamActions)) (step_dev == nullptr:
+  // use action_h_step).
+  const int64_t* step_dev = nullptr;
+  int32_t step_add = 0;
+  uint64_t action_h0 = 0;
   const double* logits = nullptr;
   const uint8_t* env_mask = nullptr;  // reinit: envs to reinit (nullptr = all)
   int32_t* episode = nullptr;         // per-env episode counter (device)

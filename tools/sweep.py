@@ -1,0 +1,64 @@
+"""C3 agent sweep and C4 env sweep (BASELINE.json configs[2], configs[3]) on
+one GPU: env-steps/s of the fused step, device-timed with CUDA events.
+
+  python tools/sweep.py [--steps K] [--out profiles/sweep_r01.json]"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2108_13976_b200 as W  # noqa: E402
+
+
+def measure(cfg, envs, steps, warmup=10, graphs=True):
+    stream = torch.cuda.current_stream()
+    ws = W.Workspace(cfg, envs, stream=stream)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, cfg.seed)
+    drv.set_graphs(graphs)
+    drv.run(warmup)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    drv.run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    drv.check()
+    geo = ws.plan.geometry()
+    ws.close()
+    return envs * steps / (ms / 1e3), ms / steps, geo
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    rows = []
+    # C3: agent sweep at 2000 envs, partial K=5, taggers = llround(A/5) (harness.cpp:823-832)
+    for A in (10, 100, 500, 1000):
+        T = max(1, min(A - 1, round(A / 5)))
+        for mode, name in ((W.PARTIAL, "partial"), (W.FULL, "full")):
+            if mode == W.FULL and A > 500:
+                continue
+            cfg = W.TagConfig(num_taggers=T, num_runners=A - T, obs_mode=mode, k_nearest=min(5, A - 1))
+            sps, ms, geo = measure(cfg, 2000, args.steps if A <= 500 else max(100, args.steps // 2))
+            rows.append(dict(sweep="C3 agents", agents=A, envs=2000, obs=name, env_steps_per_s=sps,
+                             ms_per_step=ms, per_env_step_us=1e3 * ms / 2000, geometry=geo))
+            print(json.dumps(rows[-1]))
+    # C4: env sweep, 5 agents (1 tagger + 4 runners), full obs D=19
+    for E in (1, 10, 100, 1000, 2000, 5000, 10000):
+        cfg = W.TagConfig(num_taggers=1, num_runners=4)
+        sps, ms, geo = measure(cfg, E, args.steps)
+        rows.append(dict(sweep="C4 envs", agents=5, envs=E, obs="full", env_steps_per_s=sps,
+                         ms_per_step=ms, geometry=geo))
+        print(json.dumps(rows[-1]))
+    if args.out:
+        json.dump(rows, open(args.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
