@@ -282,52 +282,66 @@ __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch
 // shell's (index-sorted) cells — no insertion network. An agent's K nearest
 // are this list minus itself. Returns the count found (< kk only if the
 // precomputed disk is exhausted; the caller then falls back per agent).
+// k-way merge of the N index-sorted cells of one shell, one cursor per cell
+// in registers, appending up to kk - found indices in increasing order.
+template <int N>
+__device__ __forceinline__ void merge_shell(const EnvSmem& s, int g, int cx, int cy, int ob,
+                                            uint16_t* out, int& found, int kk) {
+  int cur[N], end[N], head[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    cur[q] = 0;
+    end[q] = 0;
+    const int packed = c_shell_off[ob + q];
+    const int gx = cx + (packed & 0xff) - 64;
+    const int gy = cy + ((packed >> 8) & 0xff) - 64;
+    if (static_cast<unsigned>(gx) < static_cast<unsigned>(g) &&
+        static_cast<unsigned>(gy) < static_cast<unsigned>(g)) {
+      const int c2 = gy * g + gx;
+      cur[q] = s.cstart[c2];
+      end[q] = s.cstart[c2 + 1];
+    }
+    head[q] = cur[q] < end[q] ? static_cast<int>(s.items[cur[q]]) : 0x7fffffff;
+  }
+  while (found < kk) {
+    int best = head[0], bq = 0;
+#pragma unroll
+    for (int q = 1; q < N; ++q) {
+      if (head[q] < best) {
+        best = head[q];
+        bq = q;
+      }
+    }
+    if (best == 0x7fffffff) return;
+    out[found++] = static_cast<uint16_t>(best);
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      if (q == bq) {
+        ++cur[q];
+        head[q] = cur[q] < end[q] ? static_cast<int>(s.items[cur[q]]) : 0x7fffffff;
+      }
+    }
+  }
+}
+
 __device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t* out, int kk) {
   const int g = p.gc;
   const int cy = c / g, cx = c - cy * g;
   const int ns = c_num_shells;
+  // shell 0 (d2 = 0) is the cell itself: its sorted items, copied directly
   int found = 0;
-  for (int sh = 0; sh < ns && found < kk; ++sh) {
+  {
+    const int e = s.cstart[c + 1];
+    for (int t = s.cstart[c]; t < e && found < kk; ++t) out[found++] = s.items[t];
+  }
+  for (int sh = 1; sh < ns && found < kk; ++sh) {
     const int ob = c_shell_begin[sh], oe = c_shell_begin[sh + 1];
-    if (oe - ob <= 8) {
-      // k-way merge with one cursor per cell of the shell (registers).
-      int cur[8], end[8], head[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        cur[q] = 0;
-        end[q] = 0;
-        if (q < oe - ob) {
-          const int packed = c_shell_off[ob + q];
-          const int gx = cx + (packed & 0xff) - 64;
-          const int gy = cy + ((packed >> 8) & 0xff) - 64;
-          if (static_cast<unsigned>(gx) < static_cast<unsigned>(g) &&
-              static_cast<unsigned>(gy) < static_cast<unsigned>(g)) {
-            const int c2 = gy * g + gx;
-            cur[q] = s.cstart[c2];
-            end[q] = s.cstart[c2 + 1];
-          }
-        }
-        head[q] = cur[q] < end[q] ? static_cast<int>(s.items[cur[q]]) : 0x7fffffff;
-      }
-      while (found < kk) {
-        int best = head[0], bq = 0;
-#pragma unroll
-        for (int q = 1; q < 8; ++q) {
-          if (head[q] < best) {
-            best = head[q];
-            bq = q;
-          }
-        }
-        if (best == 0x7fffffff) break;
-        out[found++] = static_cast<uint16_t>(best);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (q == bq) {
-            ++cur[q];
-            head[q] = cur[q] < end[q] ? static_cast<int>(s.items[cur[q]]) : 0x7fffffff;
-          }
-        }
-      }
+    if (oe - ob == 4) {
+      merge_shell<4>(s, g, cx, cy, ob, out, found, kk);
+      continue;
+    }
+    if (oe - ob == 8) {
+      merge_shell<8>(s, g, cx, cy, ob, out, found, kk);
       continue;
     }
     int last = -1;
@@ -1157,7 +1171,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
     const int kk = p.K + 1;
     if (cell_lists) {
       for (int c = tid; c < p.ncells; c += blockDim.x) {
-        s.cfill[c] = s.cstart[c + 1] > s.cstart[c] ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
+        // only cells holding an active agent are ever looked up
+        bool any_active = false;
+        const int ce = s.cstart[c + 1];
+        for (int t = s.cstart[c]; t < ce && !any_active; ++t) any_active = s.act[s.items[t]] != 0;
+        s.cfill[c] = any_active ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
       }
       __syncthreads();
     }
@@ -1169,12 +1187,31 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
         const int cl = cell_lists ? s.cellof[a] : 0;
         if (cell_lists && s.act[a] && s.cfill[cl] == kk) {
           const uint16_t* lst = s.cellknn + cl * kk;
-          int self_pos = kk;
-          for (int t = 0; t < kk; ++t)
-            if (lst[t] == a) self_pos = t;
-          write_row<CONT, (EXACT ? MAXK : 0)>(
-              s, p, sc.step_count, a, row,
-              [&](int n) { return static_cast<int>(lst[n + (n >= self_pos ? 1 : 0)]); });
+          if constexpr (EXACT && PARTIAL) {
+            // the cell's K+1 list in registers, self dropped: nb[n] = l[n]
+            // before self's position, l[n + 1] from it on
+            int nb[MAXK];
+            bool passed = false;
+#pragma unroll
+            for (int n = 0; n < MAXK; ++n) {
+              const int ln = lst[n];
+              passed |= ln == a;
+              nb[n] = passed ? static_cast<int>(lst[n + 1]) : ln;
+            }
+            write_row<CONT, MAXK>(s, p, sc.step_count, a, row, [&](int n) {
+              int j = nb[0];
+#pragma unroll
+              for (int t = 1; t < MAXK; ++t)
+                if (t == n) j = nb[t];
+              return j;
+            });
+          } else {
+            int self_pos = kk;
+            for (int t = 0; t < kk; ++t)
+              if (lst[t] == a) self_pos = t;
+            write_row<CONT, 0>(s, p, sc.step_count, a, row,
+                               [&](int n) { return static_cast<int>(lst[n + (n >= self_pos ? 1 : 0)]); });
+          }
         } else if (PARTIAL && s.act[a]) {
           TopK<MAXK, EXACT> top;
           knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top);
