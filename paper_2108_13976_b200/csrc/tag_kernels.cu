@@ -149,6 +149,7 @@ struct EnvSmem {
   uint16_t* items;
   uint16_t* cellof;
   uint16_t* cellknn;  // lattice: per-cell top-(K+1) lists
+  uint8_t* cellact;   // grid: cell holds an active agent
 };
 
 __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
@@ -169,6 +170,7 @@ __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
   s.items = reinterpret_cast<uint16_t*>(b + p.off_items);
   s.cellof = reinterpret_cast<uint16_t*>(b + p.off_cellof);
   s.cellknn = reinterpret_cast<uint16_t*>(b + p.off_cellknn);
+  s.cellact = b + p.off_cellact;
   return s;
 }
 
@@ -241,15 +243,23 @@ __device__ void block_scan_cells(const EnvSmem& s, int n, int total, int* scratc
   if (tid == 0) s.cstart[n] = total;
 }
 
+// mark_active: also flag cells holding an active agent (used when the
+// active set is final at build time: placement); otherwise flags are zeroed
+// and set after tag resolution.
 template <bool CONT>
-__device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch) {
+__device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch,
+                           bool mark_active = false) {
   const int nthr = blockDim.x, tid = threadIdx.x;
-  for (int c = tid; c <= p.ncells; c += nthr) s.cfill[c] = 0;
+  for (int c = tid; c <= p.ncells; c += nthr) {
+    s.cfill[c] = 0;
+    if (c < p.ncells) s.cellact[c] = 0;
+  }
   __syncthreads();
   for (int a = tid; a < p.A; a += nthr) {
     const int c = cell_coord<CONT>(s.y[a], p) * p.gc + cell_coord<CONT>(s.x[a], p);
     s.cellof[a] = static_cast<uint16_t>(c);
     atomicAdd(&s.cfill[c], 1);
+    if (mark_active && s.act[a]) s.cellact[c] = 1;
   }
   __syncthreads();
   block_scan_cells(s, p.ncells, p.A, scratch);
@@ -263,6 +273,26 @@ __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch
   // produces with its serial counting sort, neighbor_grid.hpp:31-43).
   for (int c = tid; c < p.ncells; c += nthr) {
     const int b = s.cstart[c], e = s.cstart[c + 1];
+    if (e - b <= 4) {  // typical lattice cell: a 5-comparator network in registers
+      if (e - b < 2) continue;
+      int v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = b + q < e ? static_cast<int>(s.items[b + q]) : 0x7fffffff;
+      auto cx = [&](int i, int j) {
+        const int lo = min(v[i], v[j]), hi = max(v[i], v[j]);
+        v[i] = lo;
+        v[j] = hi;
+      };
+      cx(0, 1);
+      cx(2, 3);
+      cx(0, 2);
+      cx(1, 3);
+      cx(1, 2);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (b + q < e) s.items[b + q] = static_cast<uint16_t>(v[q]);
+      continue;
+    }
     for (int i = b + 1; i < e; ++i) {
       const uint16_t v = s.items[i];
       int k = i - 1;
@@ -990,6 +1020,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
         atomicAdd(&s.cred[best], 1);
       }
       const bool alive = runner && best < 0;
+      if (GRID && valid && s.act[a]) s.cellact[s.cellof[a]] = 1;  // active after resolve
       if (single) {
         const unsigned m_alive = __ballot_sync(0xffffffffu, alive);
         const unsigned m_tag = __ballot_sync(0xffffffffu, best >= 0);
@@ -1152,7 +1183,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
   // single-env CTA: `place` is CTA-uniform here (every thread has le == 0)
   if (GRID && PARTIAL && single && place) {
     __syncthreads();
-    build_grid<CONT>(s, p, scratch);
+    build_grid<CONT>(s, p, scratch, true);
   }
   __syncthreads();
   const bool lattice_ok = !CONT && GRID && p.lattice && scal[0].lattice_ok;
@@ -1172,10 +1203,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
     if (cell_lists) {
       for (int c = tid; c < p.ncells; c += blockDim.x) {
         // only cells holding an active agent are ever looked up
-        bool any_active = false;
-        const int ce = s.cstart[c + 1];
-        for (int t = s.cstart[c]; t < ce && !any_active; ++t) any_active = s.act[s.items[t]] != 0;
-        s.cfill[c] = any_active ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
+        s.cfill[c] = s.cellact[c] ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
       }
       __syncthreads();
     }
@@ -1185,7 +1213,17 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
       if (valid) {
         float* row = stage + lane * D;
         const int cl = cell_lists ? s.cellof[a] : 0;
-        if (cell_lists && s.act[a] && s.cfill[cl] == kk) {
+        if (!s.act[a]) {
+          // inactive agent: all-zero row (write_obs_row, tag_env.cpp:169-172)
+          constexpr int kVis = (EXACT && PARTIAL) ? MAXK : 0;
+          constexpr int kD = kVis * (CONT ? 7 : 4) + (CONT ? 5 : 2) + 1;
+          if constexpr (kVis > 0) {
+#pragma unroll
+            for (int f = 0; f < kD; ++f) row[f] = 0.0f;
+          } else {
+            for (int f = 0; f < D; ++f) row[f] = 0.0f;
+          }
+        } else if (cell_lists && s.cfill[cl] == kk) {
           const uint16_t* lst = s.cellknn + cl * kk;
           if constexpr (EXACT && PARTIAL) {
             // the cell's K+1 list in registers, self dropped: nb[n] = l[n]

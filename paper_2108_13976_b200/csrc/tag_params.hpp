@@ -83,6 +83,7 @@ struct TagDevConfig {
   int32_t off_y = 0, off_speed = 0, off_dir = 0, off_sin = 0, off_cos = 0;
   int32_t off_cred = 0, off_tag = 0, off_act = 0, off_tagged = 0, off_knn = 0;
   int32_t off_cstart = 0, off_cfill = 0, off_items = 0, off_cellof = 0, off_cellknn = 0;
+  int32_t off_cellact = 0;  // grid: per-cell "holds an active agent" flags
   int32_t head_bytes = 0;         // CTA header (per-env scalars + scan scratch)
   int32_t smem_bytes = 0;         // total dynamic smem per CTA
 };
