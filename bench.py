@@ -312,19 +312,25 @@ def main():
     ap.add_argument("--ref-envs-per-thread", type=int, default=4)
     ap.add_argument("--ref-inner", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # Test-only: run every rank on cuda:0 over gloo, to exercise the N>1
+    # logic (shards, barriers, max-over-ranks, stats all-reduce) on one GPU.
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
-    local_rank = env_int("LOCAL_RANK", 0)
+    local_rank = 0 if args.same_device else env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         return run_ours(args, rank, world, local_rank)
     finally:

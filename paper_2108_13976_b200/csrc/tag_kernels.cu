@@ -1303,6 +1303,47 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
       }
     }
     __syncthreads();
+    if constexpr (!PARTIAL && !CONT) {
+      if (single) {
+        // Discrete full obs (the HBM-bound C3 shapes): one warp per row. Lane
+        // l writes floats f = l + 32i; since 32 % 4 == 0 it always writes the
+        // same component (l & 3) of neighbour block f >> 2 — branch-light,
+        // 128-byte coalesced streaming stores.
+        const int nwarps = blockDim.x >> 5;
+        const int nb_f = 4 * (A - 1);
+        const int comp = lane & 3;
+        const float iw = p.inv_world;
+        const float* fsrc = comp == 0 ? s.x : s.y;
+        const uint8_t* bsrc = comp == 2 ? s.tag : s.act;
+        for (int a = warp; a < A; a += nwarps) {
+          float* dst = cta_out + static_cast<int64_t>(a) * D;
+          if (!s.act[a]) {
+            for (int f = lane; f < D; f += 32) __stcs(dst + f, 0.0f);
+            continue;
+          }
+          const float so = comp == 0 ? s.x[a] : s.y[a];
+          for (int f = lane; f < nb_f; f += 32) {
+            const int nn = f >> 2;
+            const int j = nn + (nn >= a ? 1 : 0);
+            float v;
+            if (comp < 2) {
+              v = __fmul_rn(__fsub_rn(fsrc[j], so), iw);
+            } else {
+              v = bsrc[j] ? 1.0f : 0.0f;
+            }
+            __stcs(dst + f, v);
+          }
+          if (lane < 3) {
+            const float v = lane == 0 ? __fmul_rn(s.x[a], iw)
+                          : lane == 1 ? __fmul_rn(s.y[a], iw)
+                                      : __fmul_rn(static_cast<float>(sc.step_count), p.inv_episode);
+            __stcs(dst + nb_f + lane, v);
+          }
+        }
+        goto obs_done;
+      }
+    }
+    {
     const int64_t n = static_cast<int64_t>(n_envs) * A * D;
     const int nthr = blockDim.x;
     const uint8_t* base0 = smem + p.head_bytes;
@@ -1328,7 +1369,9 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
         ++row;
       }
     }
+    }
   }
+obs_done:
 
   // Phase 8: write back the env's state.
   if (live && vec4) {
