@@ -554,6 +554,12 @@ TagLaunch Rollout::fused_launch(int64_t step) const {
   L.episode = resets_ ? resets_->episode_device() : own_episode_;
   L.env_stats = env_stats_;
   L.error = error_;
+  // Performance-analysis ablation (results invalid); see TagLaunch::ablate.
+  static const uint32_t ablate = [] {
+    const char* v = std::getenv("WDG_ABLATE");
+    return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 0)) : 0u;
+  }();
+  L.ablate = ablate;
   return L;
 }
 

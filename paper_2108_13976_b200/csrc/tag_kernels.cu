@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
               if (!CONT && p.V == 5) {
                 double z[5];
                 load_row5(L.logits, row, z);
-                act0[k] = sample5(z, u0, nonfinite);
+                act0[k] = (L.ablate & 1u) ? static_cast<int32_t>(u0 * 5.0) : sample5(z, u0, nonfinite);
               } else {
                 act0[k] = sample_row(L.logits + row * p.V, p.V, u0, nonfinite);
               }
@@ -1005,7 +1005,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
     __syncthreads();
 
     // Phase 2: bucket grid over post-move positions (NeighborGrid::build).
-    if (GRID) build_grid<CONT>(s, p, scratch);
+    if (GRID && !(L.ablate & 8u)) build_grid<CONT>(s, p, scratch);
 
     // Phase 3: resolve tags (tag_env.cpp:403-456). Counts are warp-aggregated
     // when the CTA is one env.
@@ -1203,6 +1203,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
     if (cell_lists) {
       for (int c = tid; c < p.ncells; c += blockDim.x) {
         // only cells holding an active agent are ever looked up
+        if (L.ablate & 2u) {
+          for (int t = 0; t < kk; ++t) s.cellknn[c * kk + t] = static_cast<uint16_t>(t);
+          s.cfill[c] = kk;
+          continue;
+        }
         s.cfill[c] = s.cellact[c] ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
       }
       __syncthreads();
@@ -1213,7 +1218,9 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
       if (valid) {
         float* row = stage + lane * D;
         const int cl = cell_lists ? s.cellof[a] : 0;
-        if (!s.act[a]) {
+        if (L.ablate & 4u) {
+          row[0] = static_cast<float>(a);
+        } else if (!s.act[a]) {
           // inactive agent: all-zero row (write_obs_row, tag_env.cpp:169-172)
           constexpr int kVis = (EXACT && PARTIAL) ? MAXK : 0;
           constexpr int kD = kVis * (CONT ? 7 : 4) + (CONT ? 5 : 2) + 1;

@@ -108,6 +108,10 @@ struct TagLaunch {
   // tagger_return, runner_return, tag_events, env_steps, (pad).
   double* env_stats = nullptr;
   uint32_t* error = nullptr;          // sticky error word
+  // Performance-analysis only (WDG_ABLATE env var, never set by the product,
+  // tests or bench): bit0 skip exp/sampling, bit1 skip cell K-NN, bit2 skip
+  // obs rows, bit3 skip grid build. Results are WRONG when non-zero.
+  uint32_t ablate = 0;
 };
 
 }  // namespace wdg

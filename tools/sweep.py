@@ -13,6 +13,22 @@ import torch  # noqa: E402
 import paper_2108_13976_b200 as W  # noqa: E402
 
 
+def algo_bytes(cfg):
+    """SURVEY.md §8(d) algorithmic bytes per env-step (+ continuous speed/dir)."""
+    A, C, V, D = cfg.num_agents(), cfg.action_categories(), cfg.action_choices(), cfg.obs_dim()
+    cont = 16 if cfg.variant == W.CONTINUOUS else 0
+    return A * (8 * C * V + 4 * C + 8 + 8 + cont + 1 + 2 + 4 + 1 + 4 + 4 * D) + 9
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                               "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
 def measure(cfg, envs, steps, warmup=10, graphs=True):
     stream = torch.cuda.current_stream()
     ws = W.Workspace(cfg, envs, stream=stream)
@@ -42,19 +58,33 @@ def main():
     for A in (10, 100, 500, 1000):
         T = max(1, min(A - 1, round(A / 5)))
         for mode, name in ((W.PARTIAL, "partial"), (W.FULL, "full")):
-            if mode == W.FULL and A > 500:
-                continue
             cfg = W.TagConfig(num_taggers=T, num_runners=A - T, obs_mode=mode, k_nearest=min(5, A - 1))
-            sps, ms, geo = measure(cfg, 2000, args.steps if A <= 500 else max(100, args.steps // 2))
+            n = args.steps if A <= 500 else max(100, args.steps // 2)
+            if mode == W.FULL and A >= 500:
+                n = 30  # 8 / 32 GB of observations per step: HBM-bound
+            sps, ms, geo = measure(cfg, 2000, n, warmup=3)
+            gbs = sps * algo_bytes(cfg) / 1e9
             rows.append(dict(sweep="C3 agents", agents=A, envs=2000, obs=name, env_steps_per_s=sps,
-                             ms_per_step=ms, per_env_step_us=1e3 * ms / 2000, geometry=geo))
+                             ms_per_step=ms, per_env_step_us=1e3 * ms / 2000, algo_GBps=gbs,
+                             hbm_frac=gbs / hbm_peak(), geometry=geo))
             print(json.dumps(rows[-1]))
     # C4: env sweep, 5 agents (1 tagger + 4 runners), full obs D=19
     for E in (1, 10, 100, 1000, 2000, 5000, 10000):
         cfg = W.TagConfig(num_taggers=1, num_runners=4)
         sps, ms, geo = measure(cfg, E, args.steps)
+        gbs = sps * algo_bytes(cfg) / 1e9
         rows.append(dict(sweep="C4 envs", agents=5, envs=E, obs="full", env_steps_per_s=sps,
-                         ms_per_step=ms, geometry=geo))
+                         ms_per_step=ms, algo_GBps=gbs, hbm_frac=gbs / hbm_peak(), geometry=geo))
+        print(json.dumps(rows[-1]))
+    # Continuous Tag (paper: 2000 envs x 5 agents) and larger A
+    for A, mode, name in ((5, W.FULL, "full"), (100, W.PARTIAL, "partial"), (1000, W.PARTIAL, "partial")):
+        T = max(1, min(A - 1, round(A / 5)))
+        cfg = W.TagConfig(variant=W.CONTINUOUS, num_taggers=T, num_runners=A - T, obs_mode=mode,
+                          k_nearest=min(5, A - 1))
+        sps, ms, geo = measure(cfg, 2000, args.steps if A <= 100 else max(100, args.steps // 2))
+        gbs = sps * algo_bytes(cfg) / 1e9
+        rows.append(dict(sweep="continuous", agents=A, envs=2000, obs=name, env_steps_per_s=sps,
+                         ms_per_step=ms, algo_GBps=gbs, hbm_frac=gbs / hbm_peak(), geometry=geo))
         print(json.dumps(rows[-1]))
     if args.out:
         json.dump(rows, open(args.out, "w"), indent=1)
