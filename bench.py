@@ -239,6 +239,29 @@ def run_ours(args, rank, world, local_rank):
     stats_allreduce()
     stats = stats_t.cpu().tolist()
 
+    # ---- sampler stress: the same fused step on non-uniform logits ----
+    # The headline uses the reference benchmark's zero logits, where every
+    # exp() of the softmax is exp(0) == 1 and is skipped exactly. This leg
+    # reports the step with N(0, 3^2) logits so the general
+    # sampler cost is visible next to it; not part of `value`.
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    stress_logits = torch.randn(E * A * Cc * V, dtype=torch.float64, device="cuda", generator=gen) * 3.0
+    drv.set_logits(stress_logits, stress_logits.numel())
+    stress_steps = max(1, min(args.steps, 500))
+    for _ in range(3):
+        drv.step()
+    torch.cuda.synchronize()
+    es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es0.record(stream)
+    for _ in range(stress_steps):
+        drv.step()
+    es1.record(stream)
+    torch.cuda.synchronize()
+    stress_ms = es0.elapsed_time(es1)
+    drv.set_logits(None, 0)
+    drv.check()
+    del stress_logits
+
     # ---- e2e through the C-ABI host-buffer entry point ----
     n_logits = E * A * Cc * V
     host_logits = torch.zeros(n_logits, dtype=torch.float64).pin_memory()
@@ -289,6 +312,9 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": n_logits * 8, "d2h_bytes_per_step": E * A * 4 + E,
                     "path": "wdg_rollout_step_host (pinned host logits -> fused kernel -> rewards+done)"},
+            "sampler_stress": {"logits": "N(0, 3^2), seed 1234", "steps": stress_steps,
+                               "env_steps_per_s": E * stress_steps / (stress_ms / 1e3),
+                               "ms_per_step": stress_ms / stress_steps},
             "gpu_launches": launches,
             "episode_stats": {"episodes": stats[0], "tag_events": stats[3], "env_steps": stats[4]},
             "clocks": clocks.summary(),

@@ -33,6 +33,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libwdg_b200.so")
+if os.environ.get("WDG_LIB_VARIANT"):  # tuning builds (tools/), never set by product/tests/bench
+    LIB_PATH = os.path.join(_HERE, "lib", "variants", os.environ["WDG_LIB_VARIANT"], "libwdg_b200.so")
 
 # wd_status numbering (proj/include/warp/warp_c.h:22-38) + WDG_ERR_CUDA.
 STATUS_NAMES = ["WD_OK", "WD_ERR_INVALID_ARGUMENT", "WD_ERR_DUPLICATE_NAME", "WD_ERR_SHAPE_MISMATCH",

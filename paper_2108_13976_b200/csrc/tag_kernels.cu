@@ -33,10 +33,11 @@
 namespace wdg {
 namespace {
 
-#ifndef WDG_SAMPLE_UNROLL
-#define WDG_SAMPLE_UNROLL 4
+#ifndef WDG_SAMPLE_PASS
+#define WDG_SAMPLE_PASS 2
 #endif
-constexpr int kSampleUnroll = WDG_SAMPLE_UNROLL;  // agents sampled in flight per thread
+constexpr int kSamplePass = WDG_SAMPLE_PASS;  // vec4 layout: agents whose logits are loaded per pass
+static_assert(kSamplePass == 1 || kSamplePass == 2 || kSamplePass == 4, "sample pass");
 constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
 constexpr float kTwoPiF = 6.28318530717958647692f;  // tag_env.hpp:84
 
@@ -80,7 +81,9 @@ __device__ __forceinline__ int32_t sample_row(const double* __restrict__ z, int 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i < V) {
-        ev[i] = exp(zv[i] - zmax);
+        const double d = zv[i] - zmax;  // exp(0) == 1 exactly: skip it
+        ev[i] = 1.0;
+        if (d != 0.0) ev[i] = exp(d);
         total = __dadd_rn(total, ev[i]);
       }
     }
@@ -247,8 +250,12 @@ __device__ void block_scan_cells(const EnvSmem& s, int n, int total, int* scratc
 // active set is final at build time: placement); otherwise flags are zeroed
 // and set after tag resolution.
 template <bool CONT>
+// cell_tagger: the cells are lattice points (every item of a cell sits at the
+// same position), so after the index sort s.cfill[c] is set to the cell's
+// lowest-index tagger (-1 if none): the tagger resolve credits
+// (tag_env.cpp:430-434), found once per cell instead of once per runner.
 __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch,
-                           bool mark_active = false) {
+                           bool mark_active = false, bool cell_tagger = false) {
   const int nthr = blockDim.x, tid = threadIdx.x;
   for (int c = tid; c <= p.ncells; c += nthr) {
     s.cfill[c] = 0;
@@ -274,7 +281,10 @@ __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch
   for (int c = tid; c < p.ncells; c += nthr) {
     const int b = s.cstart[c], e = s.cstart[c + 1];
     if (e - b <= 4) {  // typical lattice cell: a 5-comparator network in registers
-      if (e - b < 2) continue;
+      if (e - b < 2) {
+        if (cell_tagger) s.cfill[c] = (e > b && s.tag[s.items[b]]) ? static_cast<int>(s.items[b]) : -1;
+        continue;
+      }
       int v[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[q] = b + q < e ? static_cast<int>(s.items[b + q]) : 0x7fffffff;
@@ -288,9 +298,15 @@ __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch
       cx(0, 2);
       cx(1, 3);
       cx(1, 2);
+      int first = -1;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (b + q < e) s.items[b + q] = static_cast<uint16_t>(v[q]);
+      for (int q = 3; q >= 0; --q) {
+        if (b + q < e) {
+          s.items[b + q] = static_cast<uint16_t>(v[q]);
+          if (cell_tagger && s.tag[v[q]]) first = v[q];
+        }
+      }
+      if (cell_tagger) s.cfill[c] = first;
       continue;
     }
     for (int i = b + 1; i < e; ++i) {
@@ -301,6 +317,12 @@ __device__ void build_grid(const EnvSmem& s, const TagDevConfig& p, int* scratch
         --k;
       }
       s.items[k + 1] = v;
+    }
+    if (cell_tagger) {
+      int first = -1;
+      for (int i = b; i < e && first < 0; ++i)
+        if (s.tag[s.items[i]]) first = s.items[i];
+      s.cfill[c] = first;
     }
   }
   __syncthreads();
@@ -559,7 +581,8 @@ __device__ __forceinline__ void knn_agent(const EnvSmem& s, const TagDevConfig& 
 // Tag resolution for one active runner: resolve kernel (tag_env.cpp:403-456)
 // / TagReference::step (tag_env.cpp:546-571). Returns the credited tagger or -1.
 template <bool CONT, bool GRID>
-__device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn) {
+__device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn, bool cell_tagger) {
+  if (!CONT && GRID && cell_tagger) return s.cfill[s.cellof[rn]];
   const float rx = s.x[rn], ry = s.y[rn];
   const float bias = p.fault_bias;
   const bool exact_cell = !CONT && bias == 0.0f;
@@ -783,7 +806,11 @@ __device__ __forceinline__ int32_t sample5(const double* z, double u, bool& nonf
   double total = 0.0;
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
-    ev[i] = exp(z[i] - zmax);
+    // exp(0) == 1 exactly (glibc and CUDA alike): the row maximum, and every
+    // element of a constant row (the benchmark's uniform policy), skip exp.
+    const double d = z[i] - zmax;
+    ev[i] = 1.0;
+    if (d != 0.0) ev[i] = exp(d);
     total = __dadd_rn(total, ev[i]);
   }
   const double target = __dmul_rn(u, total);
@@ -801,12 +828,130 @@ __device__ __forceinline__ int32_t sample5(const double* z, double u, bool& nonf
   return pick;
 }
 
+// sample_from_logits for the Tag env's compile-time V (5 discrete, 3
+// continuous): the row in registers, no generic loop in the env kernel.
+template <int V>
+__device__ __forceinline__ int32_t sample_tag_row(const double* __restrict__ logits, int64_t row,
+                                                  double u, bool& nonfinite) {
+  double z[V];
+  if constexpr (V == 5) {
+    load_row5(logits, row, z);
+    return sample5(z, u, nonfinite);
+  } else {
+    const double* r = logits + row * V;
+#pragma unroll
+    for (int i = 0; i < V; ++i) z[i] = __ldg(r + i);
+    double zmax = z[0];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      nonfinite |= !isfinite(z[i]);
+      zmax = zmax < z[i] ? z[i] : zmax;
+    }
+    double ev[V];
+    double total = 0.0;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const double d = z[i] - zmax;  // exp(0) == 1 exactly: skip it
+      ev[i] = 1.0;
+      if (d != 0.0) ev[i] = exp(d);
+      total = __dadd_rn(total, ev[i]);
+    }
+    const double target = __dmul_rn(u, total);
+    double cum = 0.0;
+    int32_t pick = V - 1;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i + 1 < V; ++i) {
+      cum = __dadd_rn(cum, ev[i]);
+      if (!found && target < cum) {
+        pick = i;
+        found = true;
+      }
+    }
+    return pick;
+  }
+}
+
+// sample_from_logits (sampler.hpp:18-30) on a row already in registers.
+template <int V>
+__device__ __forceinline__ int32_t sample_regs(const double* z, double u, bool& nonfinite) {
+  if constexpr (V == 5) {
+    return sample5(z, u, nonfinite);
+  } else {
+    double zmax = z[0];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      nonfinite |= !isfinite(z[i]);
+      zmax = zmax < z[i] ? z[i] : zmax;
+    }
+    double ev[V];
+    double total = 0.0;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const double d = z[i] - zmax;  // exp(0) == 1 exactly: skip it
+      ev[i] = 1.0;
+      if (d != 0.0) ev[i] = exp(d);
+      total = __dadd_rn(total, ev[i]);
+    }
+    const double target = __dmul_rn(u, total);
+    double cum = 0.0;
+    int32_t pick = V - 1;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i + 1 < V; ++i) {
+      cum = __dadd_rn(cum, ev[i]);
+      if (!found && target < cum) {
+        pick = i;
+        found = true;
+      }
+    }
+    return pick;
+  }
+}
+
+// apply_move for one ACTIVE agent held in registers (move_discrete /
+// move_continuous, tag_env.hpp:71-100).
+template <bool CONT>
+__device__ __forceinline__ void move_regs(const TagDevConfig& p, int a, int act0, int act1, float& x,
+                                          float& y, float& sp, float& dir) {
+  if (!CONT) {
+    switch (act0) {
+      case 1: y = __fadd_rn(y, 1.0f); break;
+      case 2: y = __fsub_rn(y, 1.0f); break;
+      case 3: x = __fsub_rn(x, 1.0f); break;
+      case 4: x = __fadd_rn(x, 1.0f); break;
+      default: break;
+    }
+    x = min_ref(max_ref(x, 0.0f), p.world_hi);
+    y = min_ref(max_ref(y, 0.0f), p.world_hi);
+  } else {
+    if (act1 == 0) dir = __fsub_rn(dir, p.turn_delta);
+    if (act1 == 2) dir = __fadd_rn(dir, p.turn_delta);
+    while (dir >= kTwoPiF) dir = __fsub_rn(dir, kTwoPiF);
+    while (dir < 0.0f) dir = __fadd_rn(dir, kTwoPiF);
+    if (act0 == 0) sp = __fsub_rn(sp, p.accel_delta);
+    if (act0 == 2) sp = __fadd_rn(sp, p.accel_delta);
+    const float ms = a < p.T ? p.max_speed_tagger : p.max_speed_runner;
+    sp = min_ref(max_ref(sp, 0.0f), ms);
+    x = min_ref(max_ref(__fadd_rn(x, __fmul_rn(sp, cos_ref(dir))), 0.0f), p.world_hi);
+    y = min_ref(max_ref(__fadd_rn(y, __fmul_rn(sp, sin_ref(dir))), 0.0f), p.world_hi);
+  }
+}
+
 // ---- the env-step kernel --------------------------------------------------
 // Thread layout: tid = le * tpe + lt (le = env slot in the CTA, lt = lane in
 // the env). Per-agent loops run over `base` in warp-uniform steps so warp
 // collectives are legal; agent a = base + lt.
+// Resident CTAs per SM asked of ptxas (register cap 65536 / (threads x n)):
+// discrete K <= 8 fits 64 registers without spills -> 4 envs per SM (4 x 51.5 KB
+// of smem at C2); continuous carries 2x the per-agent state; the K > 8 top-K
+// lists live in registers and spill anyway.
+constexpr int env_min_blocks(bool cont, int maxk) {
+  return maxk > 8 ? 2 : (cont ? kMinBlocksPerSm : kMinBlocksPerSmDiscrete);
+}
+
 template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT>
-__global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_kernel(const TagDevConfig p, const TagDevArrays g,
+__global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK)) tag_env_kernel(const TagDevConfig p, const TagDevArrays g,
                                                        const TagLaunch L) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x;
@@ -820,6 +965,9 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
   const int mode = L.mode;
   const int A = p.A;
   const bool single = p.envs_per_cta == 1;  // CTA == one env: warp collectives are per env
+  // Tag action space (tag_env.hpp:48-63): discrete C=1 x V=5, continuous C=2 x V=3.
+  constexpr int kC = CONT ? 2 : 1;
+  constexpr int kV = CONT ? 3 : 5;
 
   bool live = env_ok;
   if (mode == kModeReinit && L.env_mask != nullptr && env_ok) live = L.env_mask[e] != 0;
@@ -842,7 +990,116 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
 
   // Phase 0: stage the env's agent state in shared memory.
   bool integral = true;
-  if (live && vec4) {
+  bool nonfinite = false;
+  const bool vec_step = live && vec4 && mode != kModeReinit;
+  if (vec_step) {
+    // Phases 0+1 fused per thread (each thread owns agents a0..a0+3 in both,
+    // so no barrier is needed between them): every global load of the 4
+    // agents — state, and the 160 B of f64 logits (fused) or the actions
+    // (step mode) — is issued up front, the counter hashes overlap their
+    // latency, then sample (sampler.hpp:18-30) and apply_move
+    // (tag_env.cpp:148-160) run from registers and the moved state lands in
+    // shared memory once.
+    const uint64_t h_step =
+        L.step_dev != nullptr
+            ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
+            : L.action_h_step;
+    const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
+    for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
+      const float4 x4 = *reinterpret_cast<const float4*>(g.loc_x + ga + a0);
+      const float4 y4 = *reinterpret_cast<const float4*>(g.loc_y + ga + a0);
+      const uint32_t act4 = *reinterpret_cast<const uint32_t*>(g.active + ga + a0);
+      const uint32_t tag4 = *reinterpret_cast<const uint32_t*>(g.is_tagger + ga + a0);
+      float4 sp4 = make_float4(0.f, 0.f, 0.f, 0.f), dir4 = sp4;
+      if (CONT) {
+        sp4 = *reinterpret_cast<const float4*>(g.speed + ga + a0);
+        dir4 = *reinterpret_cast<const float4*>(g.direction + ga + a0);
+      }
+      int32_t act0[4], act1[4] = {1, 1, 1, 1};
+      if (mode == kModeFused) {
+        // kSamplePass agents per pass (kSamplePass * kC * kV doubles in
+        // registers): the rows of agents a0 + P*h .. start 16-B aligned since
+        // a0 % 4 == 0 and kSamplePass * kC * kV * 8 % 16 == 0 for P in {2, 4}
+        // (P == 1 uses 8-B loads).
+        constexpr int P = kSamplePass;
+        constexpr int kRowD = P * kC * kV;
+#pragma unroll 1
+        for (int h = 0; h < 4 / P; ++h) {
+          double z[kRowD];
+          const double* lrow = L.logits + (ga + a0 + P * h) * kC * kV;
+          if constexpr (kRowD % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < kRowD / 2; ++i) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(lrow) + i);
+              z[2 * i] = v.x;
+              z[2 * i + 1] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < kRowD; ++i) z[i] = __ldg(lrow + i);
+          }
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            const int a = a0 + P * h + k;
+            const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
+            const double u0 = to_unit(absorb(absorb(h_ag, 0), 0));
+            const int32_t s0 = (L.ablate & 1u) ? static_cast<int32_t>(u0 * 5.0)
+                                               : sample_regs<kV>(z + k * kC * kV, u0, nonfinite);
+            int32_t s1 = 1;
+            if (CONT) {
+              const double u1 = to_unit(absorb(absorb(h_ag, 1), 0));
+              s1 = sample_regs<kV>(z + k * kC * kV + kV, u1, nonfinite);
+            }
+            // register arrays indexed by the runtime pass h: select, not index
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (q == P * h + k) {
+                act0[q] = s0;
+                act1[q] = s1;
+              }
+            }
+          }
+        }
+      } else if (CONT) {
+        const int4* src = reinterpret_cast<const int4*>(g.actions + (ga + a0) * 2);
+        const int4 v0 = src[0], v1 = src[1];
+        act0[0] = v0.x; act1[0] = v0.y; act0[1] = v0.z; act1[1] = v0.w;
+        act0[2] = v1.x; act1[2] = v1.y; act0[3] = v1.z; act1[3] = v1.w;
+      } else {
+        const int4 v = *reinterpret_cast<const int4*>(g.actions + ga + a0);
+        act0[0] = v.x; act0[1] = v.y; act0[2] = v.z; act0[3] = v.w;
+      }
+      if (mode == kModeFused) {
+        if (CONT) {
+          int4* dst = reinterpret_cast<int4*>(g.actions + (ga + a0) * 2);
+          dst[0] = make_int4(act0[0], act1[0], act0[1], act1[1]);
+          dst[1] = make_int4(act0[2], act1[2], act0[3], act1[3]);
+        } else {
+          *reinterpret_cast<int4*>(g.actions + ga + a0) = make_int4(act0[0], act0[1], act0[2], act0[3]);
+        }
+      }
+      float xs[4] = {x4.x, x4.y, x4.z, x4.w}, ys[4] = {y4.x, y4.y, y4.z, y4.w};
+      float sps[4] = {sp4.x, sp4.y, sp4.z, sp4.w}, dirs[4] = {dir4.x, dir4.y, dir4.z, dir4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        integral &= (xs[k] == truncf(xs[k])) && (ys[k] == truncf(ys[k])) && xs[k] >= 0.0f &&
+                    ys[k] >= 0.0f && xs[k] <= p.world_hi && ys[k] <= p.world_hi;
+        if ((act4 >> (8 * k)) & 0xffu)
+          move_regs<CONT>(p, a0 + k, act0[k], act1[k], xs[k], ys[k], sps[k], dirs[k]);
+      }
+      *reinterpret_cast<float4*>(s.x + a0) = make_float4(xs[0], xs[1], xs[2], xs[3]);
+      *reinterpret_cast<float4*>(s.y + a0) = make_float4(ys[0], ys[1], ys[2], ys[3]);
+      *reinterpret_cast<uint32_t*>(s.act + a0) = act4;
+      *reinterpret_cast<uint32_t*>(s.tag + a0) = tag4;
+      if (CONT) {
+        *reinterpret_cast<float4*>(s.sp + a0) = make_float4(sps[0], sps[1], sps[2], sps[3]);
+        *reinterpret_cast<float4*>(s.dir + a0) = make_float4(dirs[0], dirs[1], dirs[2], dirs[3]);
+      }
+      *reinterpret_cast<int4*>(s.cred + a0) = make_int4(0, 0, 0, 0);
+      *reinterpret_cast<uint32_t*>(s.tagged + a0) = 0u;
+    }
+    if (nonfinite && L.error) atomicOr(L.error, kErrNonFinite);
+  } else if (live && vec4) {
     for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
       if (mode != kModeReinit) {
         const float4 x4 = *reinterpret_cast<const float4*>(g.loc_x + ga + a0);
@@ -898,72 +1155,31 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
   } else if (env_ok && lt == 0) {
     sc.live = 0;
   }
-  __syncthreads();
-  if (!CONT && GRID && !integral) sc.lattice_ok = 0;  // benign same-value race
+  // CTA-wide AND of `integral` (only read when GRID, i.e. one env per CTA).
+  const bool all_integral = __syncthreads_and(integral) != 0;
+  if (!CONT && GRID && !all_integral && lt == 0) sc.lattice_ok = 0;
 
   bool reset_now = false;
   if (mode != kModeReinit) {
-    // Phase 1: sample (fused) + move (apply_move, tag_env.cpp:148-160).
-    if (live) {
+    // Phase 1: sample (fused) + move (apply_move, tag_env.cpp:148-160) for
+    // the per-agent (non-vec4) layout; the vec4 layout did both above.
+    if (live && !vec4) {
       const uint64_t h_step =
           L.step_dev != nullptr
               ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
               : L.action_h_step;
       const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
-      bool nonfinite = false;
-      if (vec4) {
-        for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
-          int32_t act0[4], act1[4] = {1, 1, 1, 1};
-          if (mode == kModeFused) {
-#pragma unroll kSampleUnroll
-            for (int k = 0; k < 4; ++k) {
-              const int a = a0 + k;
-              const int64_t row = (ga + a) * p.C;
-              const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
-              const double u0 = to_unit(absorb(absorb(h_ag, 0), 0));
-              if (!CONT && p.V == 5) {
-                double z[5];
-                load_row5(L.logits, row, z);
-                act0[k] = (L.ablate & 1u) ? static_cast<int32_t>(u0 * 5.0) : sample5(z, u0, nonfinite);
-              } else {
-                act0[k] = sample_row(L.logits + row * p.V, p.V, u0, nonfinite);
-              }
-              if (CONT) {
-                const double u1 = to_unit(absorb(absorb(h_ag, 1), 0));
-                act1[k] = sample_row(L.logits + (row + 1) * p.V, p.V, u1, nonfinite);
-              }
-            }
-            if (CONT) {
-              int4* dst = reinterpret_cast<int4*>(g.actions + (ga + a0) * 2);
-              dst[0] = make_int4(act0[0], act1[0], act0[1], act1[1]);
-              dst[1] = make_int4(act0[2], act1[2], act0[3], act1[3]);
-            } else {
-              *reinterpret_cast<int4*>(g.actions + ga + a0) = make_int4(act0[0], act0[1], act0[2], act0[3]);
-            }
-          } else if (CONT) {
-            const int4* src = reinterpret_cast<const int4*>(g.actions + (ga + a0) * 2);
-            const int4 v0 = src[0], v1 = src[1];
-            act0[0] = v0.x; act1[0] = v0.y; act0[1] = v0.z; act1[1] = v0.w;
-            act0[2] = v1.x; act1[2] = v1.y; act0[3] = v1.z; act1[3] = v1.w;
-          } else {
-            const int4 v = *reinterpret_cast<const int4*>(g.actions + ga + a0);
-            act0[0] = v.x; act0[1] = v.y; act0[2] = v.z; act0[3] = v.w;
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) move_agent<CONT>(s, p, a0 + k, act0[k], act1[k]);
-        }
-      }
-      for (int a = vec4 ? A : lt; a < A; a += tpe) {
+      for (int a = lt; a < A; a += tpe) {
         int32_t act0, act1 = 1;
-        const int64_t row = (ga + a) * p.C;
+        const int64_t row = (ga + a) * kC;
         if (mode == kModeFused) {
           const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
           const double u0 = to_unit(absorb(absorb(h_ag, 0), 0));
-          act0 = sample_row(L.logits + row * p.V, p.V, u0, nonfinite);
+          act0 = sample_tag_row<kV>(L.logits, row, u0, nonfinite);
           g.actions[row] = act0;
           if (CONT) {
             const double u1 = to_unit(absorb(absorb(h_ag, 1), 0));
-            act1 = sample_row(L.logits + (row + 1) * p.V, p.V, u1, nonfinite);
+            act1 = sample_tag_row<kV>(L.logits, row + 1, u1, nonfinite);
             g.actions[row + 1] = act1;
           }
         } else {
@@ -1002,10 +1218,12 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
       }
       if (nonfinite && L.error) atomicOr(L.error, kErrNonFinite);
     }
-    __syncthreads();
+    if (!vec4) __syncthreads();  // vec4: moved in phase 0, before its barrier
 
     // Phase 2: bucket grid over post-move positions (NeighborGrid::build).
-    if (GRID && !(L.ablate & 8u)) build_grid<CONT>(s, p, scratch);
+    // lattice cells are exact positions: lowest-index tagger per cell
+    const bool cell_tagger = !CONT && GRID && p.lattice && all_integral && p.fault_bias == 0.0f;
+    if (GRID && !(L.ablate & 8u)) build_grid<CONT>(s, p, scratch, false, cell_tagger);
 
     // Phase 3: resolve tags (tag_env.cpp:403-456). Counts are warp-aggregated
     // when the CTA is one env.
@@ -1013,7 +1231,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
       const int a = base + lt;
       const bool valid = live && a < A;
       const bool runner = valid && !s.tag[a] && s.act[a];
-      const int best = runner ? find_tagger<CONT, GRID>(s, p, a) : -1;
+      const int best = runner ? find_tagger<CONT, GRID>(s, p, a, cell_tagger) : -1;
       if (best >= 0) {
         s.act[a] = 0;
         s.tagged[a] = 1;
@@ -1160,8 +1378,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
         const uint8_t t = g.snap_is_tagger[ga + a];
         s.tag[a] = t;
         g.is_tagger[ga + a] = t;
-        g.actions[(ga + a) * p.C] = 0;
-        if (CONT) g.actions[(ga + a) * p.C + 1] = 0;
+        g.actions[(ga + a) * kC] = 0;
+        if (CONT) g.actions[(ga + a) * kC + 1] = 0;
       }
     }
   }
@@ -1193,7 +1411,9 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
   const int n_envs = static_cast<int>(min(static_cast<int64_t>(p.envs_per_cta), p.E - cta_env0));
   const int D = p.D;
   float* cta_out = g.obs + cta_env0 * A * D;
-  if (p.stage_obs) {
+  // K == MAXK == 5 partial rows are always staged (launch_k guarantees it),
+  // so those instantiations carry no wide-row writer.
+  if ((EXACT && PARTIAL) || p.stage_obs) {
     // Each thread builds its agent's row in a per-warp staging buffer; the
     // warp then streams the contiguous block of its rows with 16-byte stores.
     float* stage = reinterpret_cast<float*>(smem + p.off_stage) + warp * p.stage_floats;
@@ -1295,7 +1515,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, kMinBlocksPerSm) tag_env_ke
       }
       __syncwarp();
     }
-  } else {
+  } else if constexpr (!(EXACT && PARTIAL)) {
     // Wide rows (full obs, large A): K-NN into smem, then the CTA writes its
     // contiguous [envs, A, D] block cooperatively (coalesced).
     if (PARTIAL && live) {
@@ -1564,7 +1784,7 @@ cudaError_t launch_k(const TagDevConfig& p, const TagDevArrays& g, const TagLaun
   if constexpr (!PARTIAL) {
     return launch_variant<CONT, PARTIAL, GRID, 1, true>(p, g, L, st);
   } else {
-    if (p.K == 5) return launch_variant<CONT, PARTIAL, GRID, 5, true>(p, g, L, st);
+    if (p.K == 5 && p.stage_obs) return launch_variant<CONT, PARTIAL, GRID, 5, true>(p, g, L, st);
     if (p.K <= 8) return launch_variant<CONT, PARTIAL, GRID, 8, false>(p, g, L, st);
     return launch_variant<CONT, PARTIAL, GRID, 32, false>(p, g, L, st);
   }

@@ -17,7 +17,11 @@ namespace wdg {
 #define WDG_MIN_BLOCKS 3
 #endif
 inline constexpr int kMaxThreadsPerCta = WDG_MAX_THREADS;
+#ifndef WDG_MIN_BLOCKS_DISCRETE
+#define WDG_MIN_BLOCKS_DISCRETE 3
+#endif
 inline constexpr int kMinBlocksPerSm = WDG_MIN_BLOCKS;
+inline constexpr int kMinBlocksPerSmDiscrete = WDG_MIN_BLOCKS_DISCRETE;
 
 // Kernel modes (one kernel body, phase set chosen per launch; uniform per CTA).
 enum TagMode : int32_t {
