@@ -199,11 +199,27 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   }
   p.env_bytes = align16(off);
   // CTA header: per-env scalars + 64 doubles of warp scratch (scan / sums).
-  p.head_bytes = align16(p.envs_per_cta * 48 + 64 * 8);
+  p.head_bytes = align16(p.envs_per_cta * 48 + 96 * 8 + 16);  // scratch + mbarrier (tag_kernels.cu kScratchDoubles)
   int64_t total = static_cast<int64_t>(p.head_bytes) + int64_t{p.envs_per_cta} * p.env_bytes;
   if (p.stage_obs) {
     p.off_stage = static_cast<int32_t>(align16(total));
     total = p.off_stage + stage_bytes;
+  }
+  // Bulk-copy input staging (one env per CTA, A % 4 == 0): the env's f64
+  // logits rows land by one TMA bulk copy in a zone that overlays the
+  // bucket-grid and obs-staging areas, which are dead until phase 2. The
+  // zone starts at the grid block (CTA offset head + off_cstart) and grows
+  // the CTA's smem if the logits need more than those areas.
+  p.bulk_in = 0;
+  if (p.use_grid && (A % 4) == 0 && std::getenv("WDG_NO_BULK") == nullptr) {
+    const int64_t logits_bytes = int64_t{A} * p.C * p.V * 8;
+    const int64_t zone = align16(static_cast<int64_t>(p.head_bytes) + p.off_cstart);
+    const int64_t need = zone + logits_bytes;
+    if (std::max<int64_t>(total, need) <= kMaxSmem && logits_bytes % 16 == 0) {
+      p.bulk_in = 1;
+      p.off_zone = static_cast<int32_t>(zone);
+      total = std::max<int64_t>(total, need);
+    }
   }
   if (total > kMaxSmem) {
     raise(Errc::invalid_config, "device Tag path: " + std::to_string(A) +

@@ -55,6 +55,37 @@ __device__ __forceinline__ double to_unit(uint64_t h) {
   return __ull2double_rn(h >> 11) * 0x1.0p-53;
 }
 
+// ---- TMA bulk copies (cp.async.bulk) + mbarrier, raw PTX ---------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// global -> shared bulk copy, completion counted on `bar` (16-B aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
 // std::min / std::max exactly (first argument wins ties / unordered).
 __device__ __forceinline__ float min_ref(float a, float b) { return b < a ? b : a; }
 __device__ __forceinline__ float max_ref(float a, float b) { return a < b ? b : a; }
@@ -422,6 +453,20 @@ __device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t
     }
   }
   return found;
+}
+
+// Per-cell top-(K+1) lists for every cell holding an active agent (only those
+// are ever looked up); s.cfill[c] = entries found.
+__device__ __forceinline__ void build_cell_lists(const EnvSmem& s, const TagDevConfig& p, uint32_t ablate) {
+  const int kk = p.K + 1;
+  for (int c = threadIdx.x; c < p.ncells; c += blockDim.x) {
+    if (ablate & 2u) {
+      for (int t = 0; t < kk; ++t) s.cellknn[c * kk + t] = static_cast<uint16_t>(t);
+      s.cfill[c] = kk;
+      continue;
+    }
+    s.cfill[c] = s.cellact[c] ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
+  }
 }
 
 // ---- exact top-K under the (d2, index) total order ------------------------
@@ -938,6 +983,12 @@ __device__ __forceinline__ void move_regs(const TagDevConfig& p, int a, int act0
   }
 }
 
+// CTA header scratch (after the per-env scalars): doubles [0, 16) are the
+// block scan's int scratch, [16, 48) / [48, 80) the per-warp tracker sums
+// (tagger / runner), then the bulk-copy mbarrier.
+constexpr int kScratchDoubles = 96;
+constexpr int kSlotT = 16, kSlotR = 48;
+
 // ---- the env-step kernel --------------------------------------------------
 // Thread layout: tid = le * tpe + lt (le = env slot in the CTA, lt = lane in
 // the env). Per-agent loops run over `base` in warp-uniform steps so warp
@@ -1005,15 +1056,43 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
             ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
             : L.action_h_step;
     const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
+    // Bulk path (one env per CTA): one thread arms an mbarrier and issues TMA
+    // bulk copies of the env's contiguous rows — f64 logits (fused) into the
+    // zone, positions (+ speed/direction) straight into their smem arrays —
+    // so the whole 40-50 KB input is in flight at once with no registers held.
+    const bool bulk = p.bulk_in != 0;
+    const double* zone = reinterpret_cast<const double*>(smem + p.off_zone);
+    if (bulk) {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.envs_per_cta * sizeof(EnvScalars) + kScratchDoubles * 8);
+      if (tid == 0) {
+        const uint32_t rowb = static_cast<uint32_t>(A) * 4u;
+        const uint32_t lgb = mode == kModeFused ? static_cast<uint32_t>(A) * kC * kV * 8u : 0u;
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, lgb + (CONT ? 4u : 2u) * rowb);
+        if (lgb) bulk_g2s(smem + p.off_zone, L.logits + ga * kC * kV, lgb, bar);
+        bulk_g2s(s.x, g.loc_x + ga, rowb, bar);
+        bulk_g2s(s.y, g.loc_y + ga, rowb, bar);
+        if (CONT) {
+          bulk_g2s(s.sp, g.speed + ga, rowb, bar);
+          bulk_g2s(s.dir, g.direction + ga, rowb, bar);
+        }
+      }
+      __syncthreads();  // barrier initialised before anyone waits on it
+      mbar_wait(bar, 0);
+    }
     for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
-      const float4 x4 = *reinterpret_cast<const float4*>(g.loc_x + ga + a0);
-      const float4 y4 = *reinterpret_cast<const float4*>(g.loc_y + ga + a0);
+      const float4 x4 = bulk ? *reinterpret_cast<const float4*>(s.x + a0)
+                             : *reinterpret_cast<const float4*>(g.loc_x + ga + a0);
+      const float4 y4 = bulk ? *reinterpret_cast<const float4*>(s.y + a0)
+                             : *reinterpret_cast<const float4*>(g.loc_y + ga + a0);
       const uint32_t act4 = *reinterpret_cast<const uint32_t*>(g.active + ga + a0);
       const uint32_t tag4 = *reinterpret_cast<const uint32_t*>(g.is_tagger + ga + a0);
       float4 sp4 = make_float4(0.f, 0.f, 0.f, 0.f), dir4 = sp4;
       if (CONT) {
-        sp4 = *reinterpret_cast<const float4*>(g.speed + ga + a0);
-        dir4 = *reinterpret_cast<const float4*>(g.direction + ga + a0);
+        sp4 = bulk ? *reinterpret_cast<const float4*>(s.sp + a0)
+                   : *reinterpret_cast<const float4*>(g.speed + ga + a0);
+        dir4 = bulk ? *reinterpret_cast<const float4*>(s.dir + a0)
+                    : *reinterpret_cast<const float4*>(g.direction + ga + a0);
       }
       int32_t act0[4], act1[4] = {1, 1, 1, 1};
       if (mode == kModeFused) {
@@ -1026,17 +1105,32 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
 #pragma unroll 1
         for (int h = 0; h < 4 / P; ++h) {
           double z[kRowD];
-          const double* lrow = L.logits + (ga + a0 + P * h) * kC * kV;
-          if constexpr (kRowD % 2 == 0) {
+          if (bulk) {
+            const double* lrow = zone + (a0 + P * h) * kC * kV;
+            if constexpr (kRowD % 2 == 0) {
 #pragma unroll
-            for (int i = 0; i < kRowD / 2; ++i) {
-              const double2 v = __ldg(reinterpret_cast<const double2*>(lrow) + i);
-              z[2 * i] = v.x;
-              z[2 * i + 1] = v.y;
+              for (int i = 0; i < kRowD / 2; ++i) {
+                const double2 v = reinterpret_cast<const double2*>(lrow)[i];
+                z[2 * i] = v.x;
+                z[2 * i + 1] = v.y;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < kRowD; ++i) z[i] = lrow[i];
             }
           } else {
+            const double* lrow = L.logits + (ga + a0 + P * h) * kC * kV;
+            if constexpr (kRowD % 2 == 0) {
 #pragma unroll
-            for (int i = 0; i < kRowD; ++i) z[i] = __ldg(lrow + i);
+              for (int i = 0; i < kRowD / 2; ++i) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(lrow) + i);
+                z[2 * i] = v.x;
+                z[2 * i + 1] = v.y;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < kRowD; ++i) z[i] = __ldg(lrow + i);
+            }
           }
 #pragma unroll
           for (int k = 0; k < P; ++k) {
@@ -1226,7 +1320,10 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     if (GRID && !(L.ablate & 8u)) build_grid<CONT>(s, p, scratch, false, cell_tagger);
 
     // Phase 3: resolve tags (tag_env.cpp:403-456). Counts are warp-aggregated
-    // when the CTA is one env.
+    // when the CTA is one env; there "any runner still active" is all
+    // resolve_env_counters needs (tag_env.cpp:241-250), a barrier-OR.
+    bool any_alive = false;
+    const int32_t step_new = sc.step_count + 1;  // read before anyone rewrites sc
     for (int base = 0; base < A; base += tpe) {
       const int a = base + lt;
       const bool valid = live && a < A;
@@ -1238,29 +1335,37 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         atomicAdd(&s.cred[best], 1);
       }
       const bool alive = runner && best < 0;
+      any_alive |= alive;
       if (GRID && valid && s.act[a]) s.cellact[s.cellof[a]] = 1;  // active after resolve
       if (single) {
-        const unsigned m_alive = __ballot_sync(0xffffffffu, alive);
         const unsigned m_tag = __ballot_sync(0xffffffffu, best >= 0);
-        if (lane == 0 && (m_alive | m_tag)) {
-          if (m_alive) atomicAdd(&scal[0].runners_left, __popc(m_alive));
-          if (m_tag) atomicAdd(&scal[0].tags, __popc(m_tag));
-        }
+        if (lane == 0 && m_tag) atomicAdd(&scal[0].tags, __popc(m_tag));
       } else {
         if (alive) atomicAdd(&sc.runners_left, 1);
         if (best >= 0) atomicAdd(&sc.tags, 1);
       }
     }
-    __syncthreads();
     // resolve_env_counters (tag_env.cpp:241-250).
-    if (live && lt == 0) {
-      sc.step_count += 1;
-      sc.done = (sc.step_count >= p.episode_length || sc.runners_left == 0) ? 1 : 0;
+    bool done_now;
+    if (single) {
+      const bool alive_cta = __syncthreads_or(any_alive) != 0;
+      done_now = step_new >= p.episode_length || !alive_cta;
+      if (lt == 0) {  // every thread read sc.step_count before the barrier
+        sc.step_count = step_new;
+        sc.done = done_now ? 1 : 0;
+      }
+    } else {
+      __syncthreads();
+      if (live && lt == 0) {
+        sc.step_count += 1;
+        sc.done = (sc.step_count >= p.episode_length || sc.runners_left == 0) ? 1 : 0;
+      }
+      __syncthreads();
+      done_now = sc.done != 0;
     }
-    __syncthreads();
 
     // Phase 4: rewards (write_rewards_row, tag_env.cpp:252-259) + tracker.
-    reset_now = live && mode == kModeFused && L.do_reset && sc.done;
+    reset_now = live && mode == kModeFused && L.do_reset && done_now;
     const bool track = mode == kModeFused && L.track;
     double rt = 0.0, rr = 0.0;
     if (live && vec4) {
@@ -1303,15 +1408,28 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         // warp sums -> per-warp slots in `scratch` (as doubles) -> one adder
         rt = warp_sum(rt);
         rr = warp_sum(rr);
-        double* slots = reinterpret_cast<double*>(scratch);  // 2 x 32 doubles fit in head
+        double* slots = reinterpret_cast<double*>(scratch);
         if (lane == 0) {
-          slots[warp] = rt;
-          slots[32 + warp] = rr;
+          slots[kSlotT + warp] = rt;
+          slots[kSlotR + warp] = rr;
         }
       } else if (live) {
         atomicAdd(&sc.ret_tagger, rt);
         atomicAdd(&sc.ret_runner, rr);
       }
+    }
+    // Single-env CTA that does not reset: its observation inputs are final
+    // now, so the per-cell K-NN lists (lattice) / sin-cos (continuous) are
+    // built in this phase and one barrier covers rewards, tracker and them.
+    if (single && !reset_now) {
+      if (CONT) {
+        for (int a = lt; a < A; a += tpe) {
+          s.sn[a] = sin_ref(s.dir[a]);
+          s.cs[a] = cos_ref(s.dir[a]);
+        }
+      }
+      if (PARTIAL && !CONT && GRID && p.lattice && all_integral && p.stage_obs)
+        build_cell_lists(s, p, L.ablate);
     }
     __syncthreads();
     if (live && lt == 0 && track) {
@@ -1323,8 +1441,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         st = 0.0;
         sr = 0.0;
         for (int w = 0; w < (blockDim.x >> 5); ++w) {
-          st += slots[w];
-          sr += slots[32 + w];
+          st += slots[kSlotT + w];
+          sr += slots[kSlotR + w];
         }
       }
       double* es = L.env_stats + e * 8;
@@ -1383,7 +1501,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       }
     }
   }
-  __syncthreads();  // everyone has read sc.* above before it is rewritten
+  if (!single || place) __syncthreads();  // everyone has read sc.* above before it is rewritten
   if (place && lt == 0) {
     sc.step_count = 0;
     sc.done = 0;
@@ -1391,8 +1509,10 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     sc.lattice_ok = 1;  // placement is integral
   }
 
-  // Phase 6: observation inputs. Continuous: fill_sincos (tag_env.cpp:214-221).
-  if (CONT && live) {
+  // Phase 6: observation inputs. Continuous: fill_sincos (tag_env.cpp:214-221)
+  // (single-env CTAs without a reset did this in phase 4).
+  const bool early_inputs = single && mode != kModeReinit && !place;
+  if (CONT && live && !early_inputs) {
     for (int a = lt; a < A; a += tpe) {
       s.sn[a] = sin_ref(s.dir[a]);
       s.cs[a] = cos_ref(s.dir[a]);
@@ -1403,7 +1523,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     __syncthreads();
     build_grid<CONT>(s, p, scratch, true);
   }
-  __syncthreads();
+  if (!early_inputs) __syncthreads();
   const bool lattice_ok = !CONT && GRID && p.lattice && scal[0].lattice_ok;
 
   // Phase 7: K-NN + observation rows (write_obs_row, tag_env.cpp:165-212).
@@ -1420,16 +1540,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     const bool vec = ((static_cast<int64_t>(p.envs_per_cta) * A * D) & 3) == 0;
     const bool cell_lists = PARTIAL && lattice_ok;  // GRID => single env per CTA
     const int kk = p.K + 1;
-    if (cell_lists) {
-      for (int c = tid; c < p.ncells; c += blockDim.x) {
-        // only cells holding an active agent are ever looked up
-        if (L.ablate & 2u) {
-          for (int t = 0; t < kk; ++t) s.cellknn[c * kk + t] = static_cast<uint16_t>(t);
-          s.cfill[c] = kk;
-          continue;
-        }
-        s.cfill[c] = s.cellact[c] ? cell_knn(s, p, c, s.cellknn + c * kk, kk) : 0;
-      }
+    if (cell_lists && !early_inputs) {
+      build_cell_lists(s, p, L.ablate);
       __syncthreads();
     }
     for (int base = 0; base < A; base += tpe) {

@@ -10,8 +10,12 @@ for rep in range(2):
     for v in sys.argv[2:]:
         env = dict(os.environ, WDG_ABLATE="0")
         env.pop("WDG_LIB_VARIANT", None)
-        if v != "main":
-            env["WDG_LIB_VARIANT"] = v
+        lib, *kv = v.split("+")  # e.g. main+WDG_NO_BULK=1
+        if lib != "main":
+            env["WDG_LIB_VARIANT"] = lib
+        for item in kv:
+            k, val = item.split("=", 1)
+            env[k] = val
         r = subprocess.run([sys.executable, os.path.join(here, "ablate.py"), "--one", steps], env=env,
                            capture_output=True, text=True)
         print(f"rep{rep} {v:10s}: {r.stdout.strip() or r.stderr.strip()[-300:]}", flush=True)
