@@ -119,6 +119,9 @@ WDG_API const char* wdg_version(void);                 /* warp_c.h:43 */
 WDG_API const char* wdg_status_name(wdg_status status); /* warp_c.h:46 */
 WDG_API const char* wdg_last_error(void);               /* warp_c.h:49 */
 WDG_API wdg_status wdg_device_count(int32_t* out);
+/* Synchronous device -> host copy of `bytes` (inspection of device outputs
+ * such as wdg_rollout_policy_outputs). */
+WDG_API wdg_status wdg_copy_to_host(const void* device_src, void* host_dst, int64_t bytes);
 WDG_API wdg_status wdg_set_device(int32_t device);
 /* Test-only fault injection, detail::FaultHooks::tag_radius_bias
  * (proj/include/warp/tag_env.hpp:155-158): biases the device step kernels'
@@ -260,6 +263,50 @@ WDG_API wdg_status wdg_rollout_stats_device_ptr(wdg_rollout* rollout, double** o
 /* Reduce the per-env tracker slots into a caller-owned device double[8] on the
  * store's stream (e.g. a tensor that is then all-reduced over NCCL). */
 WDG_API wdg_status wdg_rollout_reduce_stats_into(wdg_rollout* rollout, double* device_out);
+
+/* ---- Policy network (proj/include/warp/policy_model.hpp) --------------- */
+/* The rollout's forward_policies (harness.cpp:445-476) on device: the
+ * reference MLP (tanh hidden layers, a linear logit head per category, a
+ * scalar value head) evaluated on the observation array in HBM. */
+typedef struct wdg_policy wdg_policy;
+/* Precision of the device forward. F64: the reference arithmetic (serial
+ * mul-then-add per output, policy_model.cpp:24-31, y = b + acc, tanh); equal
+ * to the CPU forward except where CUDA and glibc tanh round differently. BF16:
+ * bf16 operands with f32 accumulation on the tcgen05 tensor cores. */
+#define WDG_POLICY_F64 0
+#define WDG_POLICY_BF16 1
+/* PolicyDims (policy_model.hpp:20-28); check_dims (policy_model.cpp:14-21). */
+WDG_API wdg_status wdg_policy_create(int64_t obs_dim, const int64_t* hidden, int32_t num_hidden,
+                                     int64_t num_categories, int64_t num_choices, wdg_policy** out);
+WDG_API void wdg_policy_destroy(wdg_policy* policy);
+/* init_policy(seed, dims) (policy_model.cpp:107-144): Xavier-uniform from the
+ * counter RNG, zero biases; bit-identical to the reference. */
+WDG_API wdg_status wdg_policy_init(wdg_policy* policy, uint64_t seed);
+/* PolicyParams::param_count / for_each_param canonical order
+ * (policy_model.hpp:42-46, policy_model.cpp:35-56): hidden (W[out,in], b) per
+ * layer, head_w, head_b, value_w, value_b. */
+WDG_API wdg_status wdg_policy_param_count(const wdg_policy* policy, int64_t* out);
+WDG_API wdg_status wdg_policy_set_params(wdg_policy* policy, const double* host_params, int64_t count);
+WDG_API wdg_status wdg_policy_get_params(const wdg_policy* policy, double* host_params, int64_t count);
+/* forward / forward_parallel (policy_model.cpp:146-220) over agents
+ * [agent_begin, agent_end) of every env of a DEVICE f32 observation array
+ * [E, A, obs_dim]: writes DEVICE f64 logits [E, A, C*V] and values [E, A] at
+ * the same (env, agent) rows (either may be NULL). Non-finite observations ->
+ * WDG_ERR_NON_FINITE (policy_model.cpp:152-154). Synchronous. */
+WDG_API wdg_status wdg_policy_forward(const wdg_policy* policy, const float* obs, int64_t num_envs,
+                                      int64_t num_agents, int64_t agent_begin, int64_t agent_end,
+                                      double* logits, double* values, int32_t precision,
+                                      void* cuda_stream);
+/* RolloutDriver with policies (harness.cpp:428-476): each step runs the
+ * forward on the current observations, then samples, steps and resets.
+ * Taggers use `tagger`, runners `runner` (tag_policy_map, harness.cpp:395-399);
+ * the same policy twice = one shared policy (harness.cpp:586-606). NULL, NULL
+ * restores the uniform policy. Policies must outlive their use. */
+WDG_API wdg_status wdg_rollout_set_policies(wdg_rollout* rollout, const wdg_policy* tagger,
+                                            const wdg_policy* runner, int32_t precision);
+/* Device f64 logits [E,A,C*V] / values [E,A] of the last policy forward. */
+WDG_API wdg_status wdg_rollout_policy_outputs(wdg_rollout* rollout, const double** logits,
+                                              const double** values);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -140,6 +140,16 @@ def oracle_lib():
         lib.oracle_episodes.restype = C.c_int64
         lib.oracle_episodes.argtypes = [C.c_void_p, C.c_int64]
         lib.oracle_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int32]
+        I64P = C.POINTER(C.c_int64)
+        lib.oracle_policy_param_count.restype = C.c_int64
+        lib.oracle_policy_param_count.argtypes = [C.c_int64, I64P, C.c_int32, C.c_int64, C.c_int64]
+        lib.oracle_policy_init.restype = C.c_int
+        lib.oracle_policy_init.argtypes = [C.c_uint64, C.c_int64, I64P, C.c_int32, C.c_int64, C.c_int64,
+                                           C.POINTER(C.c_double), C.c_int64]
+        lib.oracle_policy_forward.restype = C.c_int
+        lib.oracle_policy_forward.argtypes = [C.POINTER(C.c_double), C.c_int64, I64P, C.c_int32, C.c_int64,
+                                              C.c_int64, C.POINTER(C.c_float), C.c_int64,
+                                              C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _oracle_lib = lib
     return _oracle_lib
 
@@ -179,6 +189,14 @@ def ref_lib():
         lib.ref_bench_sharded.restype = C.c_int
         lib.ref_bench_sharded.argtypes = [C.POINTER(TagConfigC), C.c_int64, C.c_int, C.c_int64, C.c_int64,
                                           C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        I64P = C.POINTER(C.c_int64)
+        lib.ref_policy_init.restype = C.c_int
+        lib.ref_policy_init.argtypes = [C.c_uint64, C.c_int64, I64P, C.c_int32, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_double), C.c_int64]
+        lib.ref_policy_forward.restype = C.c_int
+        lib.ref_policy_forward.argtypes = [C.POINTER(C.c_double), C.c_int64, I64P, C.c_int32, C.c_int64,
+                                           C.c_int64, C.POINTER(C.c_float), C.c_int64,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _ref_lib = lib
     return _ref_lib
 
@@ -354,3 +372,74 @@ def first_divergence(a: dict, b: dict, order=COMPARE_ORDER):
             flat = int(np.nonzero(xb[e] != yb[e])[0][0]) // x.dtype.itemsize
             return (name, e, flat)
     return None
+
+
+# ---- policy network (proj/src/policy_model.cpp) ------------------------------
+class PolicyDims:
+    """PolicyDims (policy_model.hpp:20-28)."""
+
+    def __init__(self, obs_dim, hidden=(64, 64), num_categories=1, num_choices=1):
+        self.obs_dim = int(obs_dim)
+        self.hidden = [int(h) for h in hidden]
+        self.num_categories = int(num_categories)
+        self.num_choices = int(num_choices)
+
+    def _h(self):
+        return (C.c_int64 * len(self.hidden))(*self.hidden)
+
+    def args(self):
+        return (self.obs_dim, self._h(), len(self.hidden), self.num_categories, self.num_choices)
+
+    def logits_width(self):
+        return self.num_categories * self.num_choices
+
+
+def policy_param_count(dims: PolicyDims) -> int:
+    return int(oracle_lib().oracle_policy_param_count(*dims.args()))
+
+
+def policy_init(seed: int, dims: PolicyDims, ref: bool = False) -> np.ndarray:
+    """init_policy flattened in for_each_param order: the C restatement, or
+    the reference itself (ref=True)."""
+    n = policy_param_count(dims)
+    out = np.zeros(n, dtype=np.float64)
+    fn = ref_lib().ref_policy_init if ref else oracle_lib().oracle_policy_init
+    st = fn(seed, *dims.args(), _dbl_p(out), n)
+    if st != 0:
+        raise ValueError(f"policy init failed with status {st}")
+    return out
+
+
+def policy_forward(params: np.ndarray, dims: PolicyDims, obs: np.ndarray, ref: bool = False):
+    """forward over f32 rows [rows, obs_dim] -> (logits [rows, C*V], values [rows])."""
+    obs = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1, dims.obs_dim)
+    params = np.ascontiguousarray(params, dtype=np.float64)
+    rows = obs.shape[0]
+    logits = np.zeros((rows, dims.logits_width()), dtype=np.float64)
+    values = np.zeros(rows, dtype=np.float64)
+    fn = ref_lib().ref_policy_forward if ref else oracle_lib().oracle_policy_forward
+    st = fn(_dbl_p(params), *dims.args(), obs.ctypes.data_as(C.POINTER(C.c_float)), rows,
+            _dbl_p(logits), _dbl_p(values))
+    if st != 0:
+        raise ValueError(f"policy forward failed with status {st}")
+    return logits, values
+
+
+def tag_policy_logits(world, cfg, params_tagger, params_runner, dims: PolicyDims, ref: bool = False):
+    """RolloutDriver::forward_policies (harness.cpp:445-476) on a world's
+    current observations: taggers [0, T) use params_tagger, runners the other."""
+    E = world.num_envs
+    A = cfg.num_taggers + cfg.num_runners
+    T = cfg.num_taggers
+    obs = world.pull("observations").reshape(E, A, dims.obs_dim)
+    W = dims.logits_width()
+    logits = np.zeros((E, A, W), dtype=np.float64)
+    if params_runner is None or params_runner is params_tagger:
+        lg, _ = policy_forward(params_tagger, dims, obs.reshape(-1, dims.obs_dim), ref)
+        logits[:] = lg.reshape(E, A, W)
+    else:
+        lt, _ = policy_forward(params_tagger, dims, obs[:, :T].reshape(-1, dims.obs_dim), ref)
+        lr, _ = policy_forward(params_runner, dims, obs[:, T:].reshape(-1, dims.obs_dim), ref)
+        logits[:, :T] = lt.reshape(E, T, W)
+        logits[:, T:] = lr.reshape(E, A - T, W)
+    return logits.reshape(-1)

@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "warp/policy_model.hpp"
 #include "warp/data_store.hpp"
 #include "warp/reset_manager.hpp"
 #include "warp/sampler.hpp"
@@ -295,6 +296,52 @@ __attribute__((visibility("default"))) int ref_bench_sharded(const wdg_tag_confi
     *setup_s = std::chrono::duration<double>(t1 - t0).count();
     *run_s = wall;
     *env_steps_per_s = static_cast<double>(envs_per_thread) * threads * steps / wall;
+    return 0;
+  });
+}
+
+// ---- policy network (proj/src/policy_model.cpp), test oracle only ---------
+namespace {
+warp::PolicyDims ref_dims(int64_t obs_dim, const int64_t* hidden, int32_t nh, int64_t C, int64_t V) {
+  warp::PolicyDims d;
+  d.obs_dim = obs_dim;
+  d.hidden.assign(hidden, hidden + nh);
+  d.num_categories = C;
+  d.num_choices = V;
+  return d;
+}
+}  // namespace
+
+// init_policy(seed, dims) flattened with for_each_param (policy_model.cpp:44-56).
+__attribute__((visibility("default"))) int ref_policy_init(uint64_t seed, int64_t obs_dim,
+                                                           const int64_t* hidden, int32_t nh,
+                                                           int64_t C, int64_t V, double* out,
+                                                           int64_t count) {
+  return guarded([&] {
+    const warp::PolicyParams p = warp::init_policy(seed, ref_dims(obs_dim, hidden, nh, C, V));
+    if (p.param_count() != count) throw warp::Error(warp::Errc::shape_mismatch, "param count");
+    int64_t i = 0;
+    p.for_each_param([&](const double& v) { out[i++] = v; });
+    return 0;
+  });
+}
+
+// forward_parallel(params, double(obs), rows, 1 worker) (policy_model.cpp:199-220).
+__attribute__((visibility("default"))) int ref_policy_forward(const double* params, int64_t obs_dim,
+                                                              const int64_t* hidden, int32_t nh,
+                                                              int64_t C, int64_t V, const float* obs,
+                                                              int64_t rows, double* logits,
+                                                              double* values) {
+  return guarded([&] {
+    warp::PolicyParams p = warp::init_policy(0, ref_dims(obs_dim, hidden, nh, C, V));
+    int64_t i = 0;
+    p.for_each_param([&](double& v) { v = params[i++]; });
+    std::vector<double> x(static_cast<size_t>(rows * obs_dim));
+    for (size_t k = 0; k < x.size(); ++k) x[k] = static_cast<double>(obs[k]);
+    std::vector<double> lg(static_cast<size_t>(rows * C * V)), vals(static_cast<size_t>(rows));
+    warp::forward_parallel(p, x, rows, 1, lg, vals);
+    if (logits) std::copy(lg.begin(), lg.end(), logits);
+    if (values) std::copy(vals.begin(), vals.end(), values);
     return 0;
   });
 }

@@ -557,3 +557,103 @@ int64_t oracle_episodes(const oracle_world* w, int64_t env) {
 void oracle_stats(const oracle_world* w, double* out, int32_t count) {
   for (int32_t i = 0; i < count && i < WDG_STAT_COUNT; ++i) out[i] = w->stats[i];
 }
+
+/* ---- policy network (proj/src/policy_model.cpp) -------------------------- */
+
+int64_t oracle_policy_param_count(int64_t obs_dim, const int64_t* hidden, int32_t num_hidden,
+                                  int64_t num_categories, int64_t num_choices) {
+  /* check_dims (policy_model.cpp:14-21) */
+  if (obs_dim < 1 || num_categories < 1 || num_choices < 1 || num_hidden < 1) return -1;
+  int64_t n = 0, in = obs_dim;
+  for (int32_t l = 0; l < num_hidden; ++l) {
+    if (hidden[l] < 1) return -1;
+    n += hidden[l] * in + hidden[l];
+    in = hidden[l];
+  }
+  return n + num_categories * num_choices * (in + 1) + in + 1;
+}
+
+/* xavier (policy_model.cpp:112-121): bound = sqrt(6 / (fan_in + fan_out)),
+ * w[r, c] = (2u - 1) * bound, u = uniform({stream, matrix_id, r, c, 0, 0}). */
+static void xavier(double* w, int64_t fan_out, int64_t fan_in, int64_t matrix_id, uint64_t stream) {
+  const double bound = sqrt(6.0 / (double)(fan_in + fan_out));
+  for (int64_t r = 0; r < fan_out; ++r)
+    for (int64_t c = 0; c < fan_in; ++c)
+      w[r * fan_in + c] = (2.0 * oracle_uniform(stream, matrix_id, r, c, 0, 0) - 1.0) * bound;
+}
+
+int oracle_policy_init(uint64_t seed, int64_t obs_dim, const int64_t* hidden, int32_t num_hidden,
+                       int64_t num_categories, int64_t num_choices, double* params, int64_t count) {
+  const int64_t n = oracle_policy_param_count(obs_dim, hidden, num_hidden, num_categories, num_choices);
+  if (n < 0) return 1;   /* invalid_argument */
+  if (count != n) return 3; /* shape_mismatch */
+  const uint64_t stream = oracle_substream(seed, 0x706172616d733030ULL); /* kStreamParams */
+  double* w = params;
+  int64_t in = obs_dim, id = 0;
+  for (int32_t l = 0; l < num_hidden; ++l) {
+    xavier(w, hidden[l], in, id++, stream);
+    w += hidden[l] * in;
+    for (int64_t i = 0; i < hidden[l]; ++i) *w++ = 0.0;
+    in = hidden[l];
+  }
+  for (int64_t c = 0; c < num_categories; ++c) { /* per-category logit blocks */
+    xavier(w, num_choices, in, id++, stream);
+    w += num_choices * in;
+  }
+  for (int64_t i = 0; i < num_categories * num_choices; ++i) *w++ = 0.0;
+  xavier(w, 1, in, id++, stream);
+  w += in;
+  *w = 0.0;
+  return 0;
+}
+
+int oracle_policy_forward(const double* params, int64_t obs_dim, const int64_t* hidden,
+                          int32_t num_hidden, int64_t num_categories, int64_t num_choices,
+                          const float* obs, int64_t rows, double* logits, double* values) {
+  const int64_t W = num_categories * num_choices;
+  int64_t maxw = obs_dim;
+  for (int32_t l = 0; l < num_hidden; ++l) maxw = hidden[l] > maxw ? hidden[l] : maxw;
+  for (int64_t i = 0; i < rows * obs_dim; ++i)
+    if (!isfinite((double)obs[i])) return 10; /* policy_model.cpp:152-154 */
+  double* cur = (double*)malloc(sizeof(double) * (size_t)maxw);
+  double* next = (double*)malloc(sizeof(double) * (size_t)maxw);
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t d = 0; d < obs_dim; ++d) cur[d] = (double)obs[r * obs_dim + d];
+    const double* p = params;
+    int64_t in = obs_dim;
+    for (int32_t l = 0; l < num_hidden; ++l) {
+      const int64_t out = hidden[l];
+      const double* w = p;
+      const double* b = p + out * in;
+      for (int64_t o = 0; o < out; ++o) { /* next = b; matvec_acc (policy_model.cpp:24-31) */
+        double acc = 0.0;
+        for (int64_t c = 0; c < in; ++c) acc += w[o * in + c] * cur[c];
+        next[o] = tanh(b[o] + acc);
+      }
+      p += out * in + out;
+      in = out;
+      double* t = cur;
+      cur = next;
+      next = t;
+    }
+    const double* hw = p;
+    const double* hb = hw + W * in;
+    const double* vw = hb + W;
+    const double vb = vw[in];
+    if (logits) {
+      for (int64_t o = 0; o < W; ++o) {
+        double acc = 0.0;
+        for (int64_t c = 0; c < in; ++c) acc += hw[o * in + c] * cur[c];
+        logits[r * W + o] = hb[o] + acc;
+      }
+    }
+    if (values) {
+      double v = vb; /* policy_model.cpp:192-193 */
+      for (int64_t c = 0; c < in; ++c) v += vw[c] * cur[c];
+      values[r] = v;
+    }
+  }
+  free(cur);
+  free(next);
+  return 0;
+}

@@ -63,6 +63,20 @@ void* oracle_array(oracle_world* w, const char* name, int64_t* bytes);
 int64_t oracle_episodes(const oracle_world* w, int64_t env);
 void oracle_stats(const oracle_world* w, double* out, int32_t count);
 
+/* ---- policy network (proj/src/policy_model.cpp) ------------------------ */
+/* PolicyParams::param_count (policy_model.cpp:35-42); -1 on bad dims. */
+int64_t oracle_policy_param_count(int64_t obs_dim, const int64_t* hidden, int32_t num_hidden,
+                                  int64_t num_categories, int64_t num_choices);
+/* init_policy (policy_model.cpp:107-144) into the canonical flat order. */
+int oracle_policy_init(uint64_t seed, int64_t obs_dim, const int64_t* hidden, int32_t num_hidden,
+                       int64_t num_categories, int64_t num_choices, double* params, int64_t count);
+/* forward (policy_model.cpp:146-197) of `rows` f32 observation rows (x =
+ * double(obs)); logits [rows, C*V] and values [rows] (either may be NULL).
+ * Returns 10 (non_finite) on a non-finite observation. */
+int oracle_policy_forward(const double* params, int64_t obs_dim, const int64_t* hidden,
+                          int32_t num_hidden, int64_t num_categories, int64_t num_choices,
+                          const float* obs, int64_t rows, double* logits, double* values);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,7 +70,12 @@ EXPORTED_SYMBOLS = [
     "wdg_rollout_set_fused", "wdg_rollout_set_graphs", "wdg_rollout_step", "wdg_rollout_run",
     "wdg_rollout_next_step", "wdg_rollout_check", "wdg_rollout_stats", "wdg_rollout_reset_stats",
     "wdg_rollout_stats_device_ptr", "wdg_rollout_step_host", "wdg_rollout_reduce_stats_into",
+    "wdg_policy_create", "wdg_policy_destroy", "wdg_policy_init", "wdg_policy_param_count",
+    "wdg_policy_set_params", "wdg_policy_get_params", "wdg_policy_forward", "wdg_rollout_set_policies",
+    "wdg_rollout_policy_outputs", "wdg_copy_to_host",
 ]
+
+POLICY_F64, POLICY_BF16 = 0, 1
 
 
 class WarpError(RuntimeError):
@@ -170,6 +175,16 @@ def _load():
         "wdg_rollout_stats_device_ptr": (I32, [P, C.POINTER(C.POINTER(D))]),
         "wdg_rollout_step_host": (I32, [P, P, I64, P, P]),
         "wdg_rollout_reduce_stats_into": (I32, [P, P]),
+        "wdg_policy_create": (I32, [I64, C.POINTER(I64), I32, I64, I64, C.POINTER(P)]),
+        "wdg_policy_destroy": (None, [P]),
+        "wdg_policy_init": (I32, [P, U64]),
+        "wdg_policy_param_count": (I32, [P, C.POINTER(I64)]),
+        "wdg_policy_set_params": (I32, [P, P, I64]),
+        "wdg_policy_get_params": (I32, [P, P, I64]),
+        "wdg_policy_forward": (I32, [P, P, I64, I64, I64, I64, P, P, I32, P]),
+        "wdg_rollout_set_policies": (I32, [P, P, P, I32]),
+        "wdg_rollout_policy_outputs": (I32, [P, C.POINTER(P), C.POINTER(P)]),
+        "wdg_copy_to_host": (I32, [P, P, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -187,6 +202,12 @@ def _check(status: int):
     if status != OK:
         msg = _load().wdg_last_error().decode(errors="replace")
         raise WarpError(status, msg)
+
+
+def copy_to_host(device_ptr, out: np.ndarray) -> np.ndarray:
+    """Synchronous device -> host copy into the contiguous numpy array `out`."""
+    _check(_load().wdg_copy_to_host(C.c_void_p(_ptr(device_ptr)), out.ctypes.data, out.nbytes))
+    return out
 
 
 def version() -> str:
@@ -559,6 +580,22 @@ class RolloutDriver:
     def set_logits(self, logits=None, count: int = 0):
         _check(self._lib.wdg_rollout_set_logits(self._h, C.c_void_p(_ptr(logits)), count))
 
+    def set_policies(self, tagger: Optional[Policy], runner: Optional[Policy] = None,
+                     precision: int = POLICY_F64):
+        """forward_policies (harness.cpp:445-476) on device before every step;
+        runner=None -> one shared policy; tagger=None -> uniform policy."""
+        if tagger is not None and runner is None:
+            runner = tagger
+        self._policies = (tagger, runner)  # keep alive while in use
+        _check(self._lib.wdg_rollout_set_policies(self._h, tagger._h if tagger else None,
+                                                  runner._h if runner else None, precision))
+
+    def policy_outputs(self):
+        """(logits, values) device addresses of the last policy forward."""
+        lg, vl = C.c_void_p(), C.c_void_p()
+        _check(self._lib.wdg_rollout_policy_outputs(self._h, C.byref(lg), C.byref(vl)))
+        return lg.value or 0, vl.value or 0
+
     def set_fused(self, fused: bool):
         _check(self._lib.wdg_rollout_set_fused(self._h, 1 if fused else 0))
 
@@ -606,6 +643,65 @@ class RolloutDriver:
         p = C.POINTER(C.c_double)()
         _check(self._lib.wdg_rollout_stats_device_ptr(self._h, C.byref(p)))
         return C.cast(p, C.c_void_p).value or 0
+
+
+class Policy:
+    """PolicyParams + forward (proj/include/warp/policy_model.hpp) with the
+    parameters on device: the reference MLP (tanh hidden layers, per-category
+    logit heads, a value head)."""
+
+    def __init__(self, obs_dim: int, hidden=(64, 64), num_categories: int = 1, num_choices: int = 1,
+                 seed: Optional[int] = None):
+        self._lib = _load()
+        hs = (C.c_int64 * len(hidden))(*[int(h) for h in hidden])
+        h = C.c_void_p()
+        _check(self._lib.wdg_policy_create(int(obs_dim), hs, len(hidden), int(num_categories),
+                                           int(num_choices), C.byref(h)))
+        self._h = h
+        self.obs_dim, self.hidden = int(obs_dim), [int(x) for x in hidden]
+        self.num_categories, self.num_choices = int(num_categories), int(num_choices)
+        if seed is not None:
+            self.init(seed)
+
+    @classmethod
+    def for_tag(cls, cfg: "TagConfig", hidden=(64, 64), seed: Optional[int] = None) -> "Policy":
+        return cls(cfg.obs_dim(), hidden, cfg.action_categories(), cfg.action_choices(), seed)
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wdg_policy_destroy(self._h)
+            self._h = None
+
+    def init(self, seed: int):
+        """init_policy(seed, dims) (policy_model.cpp:107-144)."""
+        _check(self._lib.wdg_policy_init(self._h, int(seed)))
+
+    def param_count(self) -> int:
+        v = C.c_int64()
+        _check(self._lib.wdg_policy_param_count(self._h, C.byref(v)))
+        return v.value
+
+    def get_params(self) -> np.ndarray:
+        out = np.zeros(self.param_count(), dtype=np.float64)
+        _check(self._lib.wdg_policy_get_params(self._h, out.ctypes.data, out.size))
+        return out
+
+    def set_params(self, params):
+        arr = np.ascontiguousarray(params, dtype=np.float64)
+        _check(self._lib.wdg_policy_set_params(self._h, arr.ctypes.data, arr.size))
+
+    def forward(self, obs, num_envs: int, num_agents: int, logits, values=None, agent_begin: int = 0,
+                agent_end: Optional[int] = None, precision: int = POLICY_F64, stream=None):
+        """forward over agents [agent_begin, agent_end) of DEVICE f32 obs
+        [E, A, obs_dim] into DEVICE f64 logits [E, A, C*V] / values [E, A]."""
+        end = num_agents if agent_end is None else agent_end
+        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        _check(self._lib.wdg_policy_forward(self._h, C.c_void_p(_ptr(obs)), num_envs, num_agents, agent_begin,
+                                            end, C.c_void_p(_ptr(logits)), C.c_void_p(_ptr(values)),
+                                            precision, st))
 
 
 class Workspace:

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "facade.hpp"
+#include "policy.hpp"
 
 struct wdg_store {
   std::unique_ptr<wdg::DataStore> impl;
@@ -19,6 +20,9 @@ struct wdg_resets {
 };
 struct wdg_rollout {
   std::unique_ptr<wdg::Rollout> impl;
+};
+struct wdg_policy {
+  std::unique_ptr<wdg::Policy> impl;
 };
 
 namespace {
@@ -402,6 +406,94 @@ wdg_status wdg_rollout_reset_stats(wdg_rollout* r) {
 
 wdg_status wdg_rollout_stats_device_ptr(wdg_rollout* r, double** out) {
   return guarded([&] { *need(out, "out") = need(r, "rollout")->impl->stats_device(); });
+}
+
+
+wdg_status wdg_policy_create(int64_t obs_dim, const int64_t* hidden, int32_t num_hidden,
+                             int64_t num_categories, int64_t num_choices, wdg_policy** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (num_hidden < 0 || (num_hidden > 0 && hidden == nullptr)) {
+      wdg::raise(wdg::Errc::invalid_argument, "policy create: bad hidden sizes");
+    }
+    wdg::PolicyDims d;
+    d.obs_dim = obs_dim;
+    d.hidden.assign(hidden, hidden + num_hidden);
+    d.num_categories = num_categories;
+    d.num_choices = num_choices;
+    auto p = std::make_unique<wdg_policy>();
+    p->impl = std::make_unique<wdg::Policy>(d);
+    *out = p.release();
+  });
+}
+
+void wdg_policy_destroy(wdg_policy* policy) { delete policy; }
+
+wdg_status wdg_policy_init(wdg_policy* policy, uint64_t seed) {
+  return guarded([&] { need(policy, "policy")->impl->init(seed); });
+}
+
+wdg_status wdg_policy_param_count(const wdg_policy* policy, int64_t* out) {
+  return guarded([&] { *need(out, "out") = need(policy, "policy")->impl->param_count(); });
+}
+
+wdg_status wdg_policy_set_params(wdg_policy* policy, const double* host_params, int64_t count) {
+  return guarded([&] { need(policy, "policy")->impl->set_params(host_params, count); });
+}
+
+wdg_status wdg_policy_get_params(const wdg_policy* policy, double* host_params, int64_t count) {
+  return guarded([&] { need(policy, "policy")->impl->get_params(host_params, count); });
+}
+
+wdg_status wdg_policy_forward(const wdg_policy* policy, const float* obs, int64_t num_envs,
+                              int64_t num_agents, int64_t agent_begin, int64_t agent_end,
+                              double* logits, double* values, int32_t precision, void* cuda_stream) {
+  return guarded([&] {
+    const wdg::Policy& p = *need(policy, "policy")->impl;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    uint32_t* err = nullptr;
+    wdg::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&err), sizeof(uint32_t), st), "policy error word");
+    wdg::cuda_check(cudaMemsetAsync(err, 0, sizeof(uint32_t), st), "policy error clear");
+    uint32_t host_err = 0;
+    try {
+      p.forward_agents(obs, num_envs, num_agents, agent_begin, agent_end, logits, values, precision, st, err);
+      wdg::cuda_check(cudaMemcpyAsync(&host_err, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, st),
+                      "policy error read");
+      wdg::cuda_check(cudaStreamSynchronize(st), "policy forward");
+    } catch (...) {
+      cudaFreeAsync(err, st);
+      throw;
+    }
+    cudaFreeAsync(err, st);
+    if (host_err & wdg::kErrNonFinite) wdg::raise(wdg::Errc::non_finite, "forward: non-finite observation");
+  });
+}
+
+wdg_status wdg_rollout_set_policies(wdg_rollout* rollout, const wdg_policy* tagger,
+                                    const wdg_policy* runner, int32_t precision) {
+  return guarded([&] {
+    need(rollout, "rollout")->impl->set_policies(tagger ? tagger->impl.get() : nullptr,
+                                                 runner ? runner->impl.get() : nullptr, precision);
+  });
+}
+
+wdg_status wdg_rollout_policy_outputs(wdg_rollout* rollout, const double** logits, const double** values) {
+  return guarded([&] {
+    const wdg::Rollout& r = *need(rollout, "rollout")->impl;
+    if (logits) *logits = r.policy_logits();
+    if (values) *values = r.policy_values();
+  });
+}
+
+wdg_status wdg_copy_to_host(const void* device_src, void* host_dst, int64_t bytes) {
+  return guarded([&] {
+    if (bytes < 0) wdg::raise(wdg::Errc::invalid_argument, "copy_to_host: negative size");
+    if (bytes == 0) return;
+    need(device_src, "device_src");
+    need(host_dst, "host_dst");
+    wdg::cuda_check(cudaMemcpy(host_dst, device_src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost),
+                    "copy_to_host");
+  });
 }
 
 }  // extern "C"

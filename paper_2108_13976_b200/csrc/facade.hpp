@@ -194,12 +194,21 @@ class ResetManager {
   int32_t ndesc_ = 0;
 };
 
+class Policy;
+
 // RolloutDriver (harness.cpp:428-505).
 class Rollout {
  public:
   Rollout(DataStore& store, TagPlan& plan, ResetManager* resets, uint64_t sample_seed);
   ~Rollout();
   void set_logits(const double* logits, int64_t count);
+  // forward_policies (harness.cpp:445-476) on device: taggers [0, T) use
+  // `tagger`, runners [T, A) use `runner` (tag_policy_map, harness.cpp:395-399);
+  // pass the same policy twice for one shared policy (check_consistency_single,
+  // harness.cpp:586-606). nullptr, nullptr restores the uniform policy.
+  void set_policies(const Policy* tagger, const Policy* runner, int32_t precision);
+  const double* policy_logits() const { return pol_logits_; }
+  const double* policy_values() const { return pol_values_; }
   void set_fused(bool f) { fused_ = f; }
   void set_graphs(bool g) { graphs_ = g; }
   void step();
@@ -215,6 +224,12 @@ class Rollout {
  private:
   TagLaunch fused_launch(int64_t step) const;
   void step_unfused();
+  void forward_policies(cudaStream_t st);
+  const Policy* pol_[2] = {nullptr, nullptr};
+  int32_t pol_prec_ = 0;
+  double* pol_logits_ = nullptr;
+  double* pol_values_ = nullptr;
+  uint64_t pol_version_ = 0, graph_pol_version_ = 0;
   bool fused_ok() const;
   DataStore& store_;
   TagPlan& plan_;

@@ -8,6 +8,7 @@
 #include <set>
 
 #include "facade.hpp"
+#include "policy.hpp"
 #include "kernels.hpp"
 
 namespace wdg {
@@ -535,6 +536,8 @@ Rollout::~Rollout() {
   }
   if (copy_) cudaStreamDestroy(copy_);
   if (zero_logits_) cudaFree(zero_logits_);
+  if (pol_logits_) cudaFree(pol_logits_);
+  if (pol_values_) cudaFree(pol_values_);
   if (env_stats_) cudaFree(env_stats_);
   if (stats_) cudaFree(stats_);
   if (error_) cudaFree(error_);
@@ -542,6 +545,10 @@ Rollout::~Rollout() {
 }
 
 void Rollout::set_logits(const double* logits, int64_t count) {
+  if (pol_[0] != nullptr) {  // explicit logits replace the device policies
+    pol_[0] = pol_[1] = nullptr;
+    ++pol_version_;
+  }
   if (logits == nullptr) {
     logits_ = zero_logits_;
     return;
@@ -579,6 +586,51 @@ TagLaunch Rollout::fused_launch(int64_t step) const {
   return L;
 }
 
+void Rollout::set_policies(const Policy* tagger, const Policy* runner, int32_t precision) {
+  if ((tagger == nullptr) != (runner == nullptr)) {
+    raise(Errc::invalid_argument, "set_policies: give both policies or neither");
+  }
+  const TagDevConfig& p = plan_.dev();
+  if (tagger != nullptr) {
+    for (const Policy* q : {tagger, runner}) {
+      const PolicyDims& d = q->dims();
+      if (d.obs_dim != p.D || d.num_categories != p.C || d.num_choices != p.V) {
+        raise(Errc::shape_mismatch, "set_policies: policy dims do not match the Tag config (obs_dim " +
+                                        std::to_string(p.D) + ", C " + std::to_string(p.C) + ", V " +
+                                        std::to_string(p.V) + ")");
+      }
+    }
+    if (precision != kPolicyF64 && precision != kPolicyBF16) {
+      raise(Errc::invalid_argument, "set_policies: unknown precision");
+    }
+    if (pol_logits_ == nullptr) {
+      const size_t n = static_cast<size_t>(p.E) * p.A;
+      cuda_check(cudaMalloc(&pol_logits_, n * p.C * p.V * sizeof(double)), "cudaMalloc(policy logits)");
+      cuda_check(cudaMalloc(&pol_values_, n * sizeof(double)), "cudaMalloc(policy values)");
+    }
+    logits_ = pol_logits_;
+  } else {
+    logits_ = zero_logits_;
+  }
+  pol_[0] = tagger;
+  pol_[1] = runner;
+  pol_prec_ = precision;
+  ++pol_version_;
+}
+
+// forward_policies (harness.cpp:445-476): obs (already in HBM) -> f64 logits.
+void Rollout::forward_policies(cudaStream_t st) {
+  if (pol_[0] == nullptr) return;
+  const TagDevConfig& p = plan_.dev();
+  const float* obs = static_cast<const float*>(store_.device_ptr(store_.handle(kObservations)));
+  if (pol_[0] == pol_[1]) {
+    pol_[0]->forward_agents(obs, p.E, p.A, 0, p.A, pol_logits_, pol_values_, pol_prec_, st, error_);
+  } else {
+    pol_[0]->forward_agents(obs, p.E, p.A, 0, p.T, pol_logits_, pol_values_, pol_prec_, st, error_);
+    pol_[1]->forward_agents(obs, p.E, p.A, p.T, p.A, pol_logits_, pol_values_, pol_prec_, st, error_);
+  }
+}
+
 void Rollout::step_unfused() {
   const TagDevConfig& p = plan_.dev();
   const uint64_t h_step = host_absorb(h_actions0_, static_cast<uint64_t>(t_));
@@ -592,6 +644,7 @@ void Rollout::step_unfused() {
 }
 
 void Rollout::step() {
+  forward_policies(store_.stream());
   if (fused_ok()) {
     plan_.launch(fused_launch(t_));
   } else {
@@ -605,6 +658,7 @@ void Rollout::step_host(const double* host_logits, int64_t count, float* host_re
   const TagDevConfig& p = plan_.dev();
   const int64_t expected = int64_t{p.E} * p.A * p.C * p.V;
   if (host_logits == nullptr) raise(Errc::invalid_argument, "step_host: null logits");
+  if (pol_[0] != nullptr) raise(Errc::state_error, "step_host: the rollout samples from device policies");
   if (count != expected) {
     raise(Errc::shape_mismatch, "step_host: logits size " + std::to_string(count) + ", expected " +
                                     std::to_string(expected));
@@ -672,6 +726,14 @@ void Rollout::build_graph() {
   cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
   cudaError_t err = cudaSuccess;
   for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
+    if (pol_[0] != nullptr) {
+      try {
+        forward_policies(cap);
+      } catch (const Error&) {
+        err = cudaErrorUnknown;
+        break;
+      }
+    }
     TagLaunch L = fused_launch(0);
     L.step_dev = step_dev_;
     L.step_add = i;
@@ -689,6 +751,7 @@ void Rollout::build_graph() {
   cudaGraphDestroy(graph);
   cuda_check(err, "graph instantiate");
   graph_logits_ = logits_;
+  graph_pol_version_ = pol_version_;
   graph_bias_ = fault_tag_radius_bias();
   graph_stream_ = st;
 }
@@ -696,7 +759,8 @@ void Rollout::build_graph() {
 void Rollout::run(int64_t steps) {
   if (steps < 0) raise(Errc::invalid_argument, "rollout run: steps must be >= 0");
   if (graphs_ && fused_ok() && steps >= kGraphSteps) {
-    if (graph_exec_ == nullptr || graph_logits_ != logits_ || graph_bias_ != fault_tag_radius_bias() ||
+    if (graph_exec_ == nullptr || graph_logits_ != logits_ || graph_pol_version_ != pol_version_ ||
+        graph_bias_ != fault_tag_radius_bias() ||
         graph_stream_ != store_.stream()) {
       build_graph();
     }
