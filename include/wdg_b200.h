@@ -304,6 +304,10 @@ WDG_API wdg_status wdg_policy_forward(const wdg_policy* policy, const float* obs
  * restores the uniform policy. Policies must outlive their use. */
 WDG_API wdg_status wdg_rollout_set_policies(wdg_rollout* rollout, const wdg_policy* tagger,
                                             const wdg_policy* runner, int32_t precision);
+/* Keep the last forward's f64 logits (always kept for F64, which samples
+ * from them) and values in device buffers (default off: the BF16 path then
+ * stores only the sampled actions). */
+WDG_API wdg_status wdg_rollout_set_keep_policy_outputs(wdg_rollout* rollout, int32_t keep);
 /* Device f64 logits [E,A,C*V] / values [E,A] of the last policy forward. */
 WDG_API wdg_status wdg_rollout_policy_outputs(wdg_rollout* rollout, const double** logits,
                                               const double** values);

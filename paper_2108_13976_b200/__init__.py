@@ -72,7 +72,7 @@ EXPORTED_SYMBOLS = [
     "wdg_rollout_stats_device_ptr", "wdg_rollout_step_host", "wdg_rollout_reduce_stats_into",
     "wdg_policy_create", "wdg_policy_destroy", "wdg_policy_init", "wdg_policy_param_count",
     "wdg_policy_set_params", "wdg_policy_get_params", "wdg_policy_forward", "wdg_rollout_set_policies",
-    "wdg_rollout_policy_outputs", "wdg_copy_to_host",
+    "wdg_rollout_policy_outputs", "wdg_copy_to_host", "wdg_rollout_set_keep_policy_outputs",
 ]
 
 POLICY_F64, POLICY_BF16 = 0, 1
@@ -185,6 +185,7 @@ def _load():
         "wdg_rollout_set_policies": (I32, [P, P, P, I32]),
         "wdg_rollout_policy_outputs": (I32, [P, C.POINTER(P), C.POINTER(P)]),
         "wdg_copy_to_host": (I32, [P, P, I64]),
+        "wdg_rollout_set_keep_policy_outputs": (I32, [P, I32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -589,6 +590,9 @@ class RolloutDriver:
         self._policies = (tagger, runner)  # keep alive while in use
         _check(self._lib.wdg_rollout_set_policies(self._h, tagger._h if tagger else None,
                                                   runner._h if runner else None, precision))
+
+    def set_keep_policy_outputs(self, keep: bool):
+        _check(self._lib.wdg_rollout_set_keep_policy_outputs(self._h, 1 if keep else 0))
 
     def policy_outputs(self):
         """(logits, values) device addresses of the last policy forward."""

@@ -477,6 +477,10 @@ wdg_status wdg_rollout_set_policies(wdg_rollout* rollout, const wdg_policy* tagg
   });
 }
 
+wdg_status wdg_rollout_set_keep_policy_outputs(wdg_rollout* rollout, int32_t keep) {
+  return guarded([&] { need(rollout, "rollout")->impl->set_keep_policy_outputs(keep != 0); });
+}
+
 wdg_status wdg_rollout_policy_outputs(wdg_rollout* rollout, const double** logits, const double** values) {
   return guarded([&] {
     const wdg::Rollout& r = *need(rollout, "rollout")->impl;

@@ -207,6 +207,12 @@ class Rollout {
   // pass the same policy twice for one shared policy (check_consistency_single,
   // harness.cpp:586-606). nullptr, nullptr restores the uniform policy.
   void set_policies(const Policy* tagger, const Policy* runner, int32_t precision);
+  // Keep the policy's f64 logits (bf16 path) and values in device buffers
+  // readable through policy_logits()/policy_values() (default off).
+  void set_keep_policy_outputs(bool keep) {
+    keep_outputs_ = keep;
+    ++pol_version_;
+  }
   const double* policy_logits() const { return pol_logits_; }
   const double* policy_values() const { return pol_values_; }
   void set_fused(bool f) { fused_ = f; }
@@ -224,12 +230,14 @@ class Rollout {
  private:
   TagLaunch fused_launch(int64_t step) const;
   void step_unfused();
-  void forward_policies(cudaStream_t st);
+  void forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add);
+  bool policy_samples() const { return pol_[0] != nullptr && pol_prec_ == 1; }  // kPolicyBF16
   const Policy* pol_[2] = {nullptr, nullptr};
   int32_t pol_prec_ = 0;
   double* pol_logits_ = nullptr;
   double* pol_values_ = nullptr;
   uint64_t pol_version_ = 0, graph_pol_version_ = 0;
+  bool keep_outputs_ = false;
   bool fused_ok() const;
   DataStore& store_;
   TagPlan& plan_;

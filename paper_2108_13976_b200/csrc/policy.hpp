@@ -34,6 +34,17 @@ enum PolicyPrecision : int32_t {
   kPolicyBF16 = 1,
 };
 
+// Counter-RNG keys of sample_actions (sampler.cpp:31-39) for a fused
+// forward+sample: h_step = absorb(mix64(substream(seed, kStreamActions)), t),
+// or, under graph replay, t = *step_dev + step_add hashed from h0 on device.
+struct SampleKeys {
+  int64_t env_offset = 0;
+  uint64_t h_step = 0;
+  const int64_t* step_dev = nullptr;
+  int32_t step_add = 0;
+  uint64_t h0 = 0;
+};
+
 class Policy {
  public:
   explicit Policy(PolicyDims dims);
@@ -62,6 +73,14 @@ class Policy {
   // the reference raises non_finite, policy_model.cpp:152-154).
   void forward_agents(const float* obs, int64_t E, int64_t A, int64_t a0, int64_t a1, double* logits,
                       double* values, int32_t precision, cudaStream_t st, uint32_t* error) const;
+  // kPolicyBF16 forward fused with sample_actions: writes the sampled actions
+  // [E, A, C] (actions may be nullptr) and optionally f64 logits / values.
+  void forward_sample_bf16(const float* obs, int64_t E, int64_t A, int64_t a0, int64_t a1, int32_t* actions,
+                           double* logits, double* values, const SampleKeys& keys, cudaStream_t st,
+                           uint32_t* error) const;
+  // The bf16 tensor-core path covers the reference default dims: hidden
+  // {64, 64}, C*V <= 7, obs_dim <= 128.
+  bool bf16_supported() const;
 
  private:
   void upload() const;  // lazy host -> device copy (mutable caches)
@@ -71,6 +90,7 @@ class Policy {
   mutable bool dirty_ = true;
   mutable double* dparams_ = nullptr;    // canonical order
   mutable double* dparams_t_ = nullptr;  // transposed weights for the f64 kernel
+  mutable uint8_t* dimage_ = nullptr;    // bf16 smem image of the tensor-core kernel
 };
 
 }  // namespace wdg

@@ -573,7 +573,7 @@ TagLaunch Rollout::fused_launch(int64_t step) const {
   L.do_reset = (resets_ != nullptr && resets_->auto_enabled()) ? 1 : 0;
   L.track = 1;
   L.action_h_step = host_absorb(h_actions0_, static_cast<uint64_t>(step));
-  L.logits = logits_;
+  L.logits = policy_samples() ? nullptr : logits_;  // bf16 policies sampled already
   L.episode = resets_ ? resets_->episode_device() : own_episode_;
   L.env_stats = env_stats_;
   L.error = error_;
@@ -603,6 +603,9 @@ void Rollout::set_policies(const Policy* tagger, const Policy* runner, int32_t p
     if (precision != kPolicyF64 && precision != kPolicyBF16) {
       raise(Errc::invalid_argument, "set_policies: unknown precision");
     }
+    if (precision == kPolicyBF16 && (!tagger->bf16_supported() || !runner->bf16_supported())) {
+      raise(Errc::invalid_config, "set_policies: the bf16 tensor-core path needs hidden {64, 64}");
+    }
     if (pol_logits_ == nullptr) {
       const size_t n = static_cast<size_t>(p.E) * p.A;
       cuda_check(cudaMalloc(&pol_logits_, n * p.C * p.V * sizeof(double)), "cudaMalloc(policy logits)");
@@ -618,23 +621,45 @@ void Rollout::set_policies(const Policy* tagger, const Policy* runner, int32_t p
   ++pol_version_;
 }
 
-// forward_policies (harness.cpp:445-476): obs (already in HBM) -> f64 logits.
-void Rollout::forward_policies(cudaStream_t st) {
+// forward_policies (harness.cpp:445-476): obs (already in HBM) -> f64 logits,
+// or (bf16) the tensor-core forward fused with sample_actions for step t ->
+// sampled actions, which the fused env launch then reads (L.logits == nullptr).
+void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add) {
   if (pol_[0] == nullptr) return;
   const TagDevConfig& p = plan_.dev();
   const float* obs = static_cast<const float*>(store_.device_ptr(store_.handle(kObservations)));
+  // f64 logits are the sampler's input (always written); bf16 samples in the
+  // epilogue and stores logits / values only when asked to keep them.
+  double* lg = (pol_prec_ == kPolicyBF16 && !keep_outputs_) ? nullptr : pol_logits_;
+  double* vl = keep_outputs_ ? pol_values_ : nullptr;
+  if (pol_prec_ == kPolicyBF16) {
+    SampleKeys k;
+    k.env_offset = p.env_offset;
+    k.h_step = host_absorb(h_actions0_, static_cast<uint64_t>(step));
+    k.step_dev = step_dev;
+    k.step_add = step_add;
+    k.h0 = h_actions0_;
+    int32_t* act = static_cast<int32_t*>(store_.device_ptr(store_.handle(kSampledActions)));
+    if (pol_[0] == pol_[1]) {
+      pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.A, act, lg, vl, k, st, error_);
+    } else {
+      pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.T, act, lg, vl, k, st, error_);
+      pol_[1]->forward_sample_bf16(obs, p.E, p.A, p.T, p.A, act, lg, vl, k, st, error_);
+    }
+    return;
+  }
   if (pol_[0] == pol_[1]) {
-    pol_[0]->forward_agents(obs, p.E, p.A, 0, p.A, pol_logits_, pol_values_, pol_prec_, st, error_);
+    pol_[0]->forward_agents(obs, p.E, p.A, 0, p.A, lg, vl, pol_prec_, st, error_);
   } else {
-    pol_[0]->forward_agents(obs, p.E, p.A, 0, p.T, pol_logits_, pol_values_, pol_prec_, st, error_);
-    pol_[1]->forward_agents(obs, p.E, p.A, p.T, p.A, pol_logits_, pol_values_, pol_prec_, st, error_);
+    pol_[0]->forward_agents(obs, p.E, p.A, 0, p.T, lg, vl, pol_prec_, st, error_);
+    pol_[1]->forward_agents(obs, p.E, p.A, p.T, p.A, lg, vl, pol_prec_, st, error_);
   }
 }
 
 void Rollout::step_unfused() {
   const TagDevConfig& p = plan_.dev();
   const uint64_t h_step = host_absorb(h_actions0_, static_cast<uint64_t>(t_));
-  cuda_check(launch_sample(logits_,
+  if (!policy_samples()) cuda_check(launch_sample(logits_,
                            static_cast<int32_t*>(store_.device_ptr(store_.handle(kSampledActions))),
                            int64_t{p.E} * p.A * p.C, p.A, p.C, p.V, p.env_offset, h_step,
                            store_.stream()),
@@ -644,7 +669,7 @@ void Rollout::step_unfused() {
 }
 
 void Rollout::step() {
-  forward_policies(store_.stream());
+  forward_policies(store_.stream(), t_, nullptr, 0);
   if (fused_ok()) {
     plan_.launch(fused_launch(t_));
   } else {
@@ -728,7 +753,7 @@ void Rollout::build_graph() {
   for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
     if (pol_[0] != nullptr) {
       try {
-        forward_policies(cap);
+        forward_policies(cap, 0, step_dev_, i);
       } catch (const Error&) {
         err = cudaErrorUnknown;
         break;

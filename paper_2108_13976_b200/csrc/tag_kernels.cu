@@ -1015,6 +1015,10 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   const bool env_ok = le < p.envs_per_cta && e < p.E;
   const int mode = L.mode;
   const int A = p.A;
+  // Fused steps sample from L.logits; with L.logits == nullptr the actions are
+  // already in the store (sampled by the policy kernel) and are read like the
+  // step mode does.
+  const bool sample_here = mode == kModeFused && L.logits != nullptr;
   const bool single = p.envs_per_cta == 1;  // CTA == one env: warp collectives are per env
   // Tag action space (tag_env.hpp:48-63): discrete C=1 x V=5, continuous C=2 x V=3.
   constexpr int kC = CONT ? 2 : 1;
@@ -1066,7 +1070,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.envs_per_cta * sizeof(EnvScalars) + kScratchDoubles * 8);
       if (tid == 0) {
         const uint32_t rowb = static_cast<uint32_t>(A) * 4u;
-        const uint32_t lgb = mode == kModeFused ? static_cast<uint32_t>(A) * kC * kV * 8u : 0u;
+        const uint32_t lgb = sample_here ? static_cast<uint32_t>(A) * kC * kV * 8u : 0u;
         mbar_init(bar, 1);
         mbar_expect_tx(bar, lgb + (CONT ? 4u : 2u) * rowb);
         if (lgb) bulk_g2s(smem + p.off_zone, L.logits + ga * kC * kV, lgb, bar);
@@ -1095,7 +1099,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
                     : *reinterpret_cast<const float4*>(g.direction + ga + a0);
       }
       int32_t act0[4], act1[4] = {1, 1, 1, 1};
-      if (mode == kModeFused) {
+      if (sample_here) {
         // kSamplePass agents per pass (kSamplePass * kC * kV doubles in
         // registers): the rows of agents a0 + P*h .. start 16-B aligned since
         // a0 % 4 == 0 and kSamplePass * kC * kV * 8 % 16 == 0 for P in {2, 4}
@@ -1163,7 +1167,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         const int4 v = *reinterpret_cast<const int4*>(g.actions + ga + a0);
         act0[0] = v.x; act0[1] = v.y; act0[2] = v.z; act0[3] = v.w;
       }
-      if (mode == kModeFused) {
+      if (sample_here) {
         if (CONT) {
           int4* dst = reinterpret_cast<int4*>(g.actions + (ga + a0) * 2);
           dst[0] = make_int4(act0[0], act1[0], act0[1], act1[1]);
@@ -1266,7 +1270,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       for (int a = lt; a < A; a += tpe) {
         int32_t act0, act1 = 1;
         const int64_t row = (ga + a) * kC;
-        if (mode == kModeFused) {
+        if (sample_here) {
           const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
           const double u0 = to_unit(absorb(absorb(h_ag, 0), 0));
           act0 = sample_tag_row<kV>(L.logits, row, u0, nonfinite);

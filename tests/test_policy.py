@@ -177,3 +177,103 @@ def test_policy_rollout_matches_oracle(name, fused):
             assert rel_err(got, logits) <= LOGIT_RTOL, f"{name} step {t}: policy logits"
     drv.check()
     ws.close()
+
+
+# ---- bf16 tensor-core path -----------------------------------------------------
+BF16_EMU_ATOL = 5e-3   # vs a torch fp32 forward that rounds operands/activations to bf16 like the kernel
+BF16_F32_ATOL = 6e-2   # vs the plain torch fp32 forward of the same parameters (bf16 quantisation error)
+
+
+def torch_mlp(torch, params, dims, obs, emulate_bf16):
+    """Plain PyTorch fp32 forward of the reference MLP (policy_model.cpp:146-197)."""
+    p = torch.as_tensor(params, dtype=torch.float32)
+    q = (lambda t: t.to(torch.bfloat16).to(torch.float32)) if emulate_bf16 else (lambda t: t)
+    D, W = dims.obs_dim, dims.logits_width()
+    off = 0
+    x = q(torch.as_tensor(obs, dtype=torch.float32))
+    in_w = D
+    for h in dims.hidden:
+        w = p[off:off + h * in_w].reshape(h, in_w)
+        b = p[off + h * in_w: off + h * in_w + h]
+        x = q(torch.tanh(x @ q(w).T + b))
+        off += h * in_w + h
+        in_w = h
+    hw = p[off:off + W * in_w].reshape(W, in_w)
+    hb = p[off + W * in_w: off + W * in_w + W]
+    vw = p[off + W * in_w + W: off + W * in_w + W + in_w]
+    vb = p[off + W * in_w + W + in_w]
+    return (x @ q(hw).T + hb).numpy(), (x @ q(vw) + vb).numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", DIMS[:2], ids=lambda d: f"D{d.obs_dim}")
+def test_device_bf16_forward_matches_torch(dims):
+    torch = _gpu()
+    rng = np.random.default_rng(5)
+    E, A = 53, 37  # 1961 rows: 16 tiles of 128, the last partial
+    params = O.policy_init(4, dims) + rng.normal(0, 0.05, O.policy_param_count(dims))
+    obs = rng.uniform(-1, 1, (E, A, dims.obs_dim)).astype(np.float32)
+    p = W.Policy(dims.obs_dim, dims.hidden, dims.num_categories, dims.num_choices)
+    p.set_params(params)
+    Wd = dims.logits_width()
+    d_lg = torch.full((E, A, Wd), -7.0, dtype=torch.float64, device="cuda")
+    d_v = torch.full((E, A), -7.0, dtype=torch.float64, device="cuda")
+    p.forward(torch.from_numpy(obs).cuda(), E, A, d_lg, d_v, 0, 10, precision=W.POLICY_BF16)
+    p.forward(torch.from_numpy(obs).cuda(), E, A, d_lg, d_v, 10, A, precision=W.POLICY_BF16)
+    lg = d_lg.cpu().numpy().reshape(-1, Wd)
+    v = d_v.cpu().numpy().reshape(-1)
+    el, ev = torch_mlp(torch, params, dims, obs.reshape(-1, dims.obs_dim), True)
+    fl, fv = torch_mlp(torch, params, dims, obs.reshape(-1, dims.obs_dim), False)
+    assert np.max(np.abs(lg - el)) <= BF16_EMU_ATOL, np.max(np.abs(lg - el))
+    assert np.max(np.abs(v - ev)) <= BF16_EMU_ATOL
+    assert np.max(np.abs(lg - fl)) <= BF16_F32_ATOL, np.max(np.abs(lg - fl))
+    assert np.max(np.abs(v - fv)) <= BF16_F32_ATOL
+    p.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("shared", [True, False])
+def test_bf16_policy_rollout_samples_its_logits_exactly(fused, shared):
+    """The bf16 kernel samples in its epilogue from f64(its f32 logits): the
+    oracle stepped with those very logits (sampler.cpp + TagReference) must
+    reproduce the device store bit-for-bit; the actions also agree with the
+    f64 policy's for the overwhelming majority of agents."""
+    _gpu()
+    kw = dict(num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, episode_length=25, grid_size=12, seed=5)
+    E = 10
+    oc = O.make_config(**kw)
+    dc = W.TagConfig(**{f: getattr(oc, f) for f, _ in O.TagConfigC._fields_})
+    dims = O.PolicyDims(dc.obs_dim(), (64, 64), 1, 5)
+    dev_t = W.Policy.for_tag(dc, seed=11)
+    dev_r = dev_t if shared else W.Policy.for_tag(dc, seed=12)
+    pt = O.policy_init(11, dims)
+    pr = pt if shared else O.policy_init(12, dims)
+    ws = W.Workspace(dc, E)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, kw["seed"])
+    drv.set_fused(fused)
+    drv.set_policies(dev_t, None if shared else dev_r, W.POLICY_BF16)
+    drv.set_keep_policy_outputs(True)
+    ow = O.OracleWorld(oc, E)
+    agree = total = 0
+    for t in range(40):
+        f64_logits = O.tag_policy_logits(ow, oc, pt, pr, dims)
+        f64_actions = ow.pull("sampled_actions").copy()
+        drv.step()
+        lg_ptr, _ = drv.policy_outputs()
+        dev_logits = W.copy_to_host(lg_ptr, np.zeros(f64_logits.size, dtype=np.float64))
+        assert np.max(np.abs(dev_logits - f64_logits)) <= BF16_F32_ATOL
+        # what the f64 policy would have sampled at this step
+        probe = O.OracleWorld(oc, E)  # sampling depends only on (seed, step, env, agent, logits)
+        probe.sample(t, kw["seed"], f64_logits)
+        want = probe.pull("sampled_actions").copy()
+        del probe, f64_actions
+        ow.rollout(t, 1, kw["seed"], dev_logits)
+        got = ws.store.pull("sampled_actions")
+        agree += int(np.sum(got == want))
+        total += got.size
+        d = O.first_divergence({n: ws.store.pull(n) for n in ow.layout}, ow.snapshot())
+        assert d is None, f"step {t}: first divergence {d}"
+    drv.check()
+    assert agree / total >= 0.95, agree / total
+    ws.close()

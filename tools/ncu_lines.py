@@ -43,9 +43,10 @@ def sass_metrics(rep):
 def line_table():
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(SO)], cwd=d, capture_output=True)
-    cub = [f for f in os.listdir(d) if f.startswith("tag_kernels")][0]
-    txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True,
-                         text=True).stdout
+    txt = ""
+    for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):
+        txt += subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True,
+                              text=True).stdout + "\n"
     funcs = {}
     fn, line = None, None
     for ln in txt.splitlines():
@@ -77,9 +78,10 @@ def main():
             continue
         # match function by template args
         targs = re.findall(r"\((bool|int)\)(\w+)", kname)
-        mangled = [f for f in funcs if "tag_env_kernel" in f]
+        base_name = re.findall(r"(\w+)(?:<\(|\()", kname)[0]
+        mangled = [f for f in funcs if base_name in f]
         sig = "".join((f"Lb{a}E" if t == "bool" else f"Li{a}E") for t, a in targs)
-        cand = [f for f in mangled if sig in f.replace("ILb", "Lb")] or mangled
+        cand = [f for f in mangled if sig in f.replace("ILb", "Lb").replace("ILi", "Li")] or mangled
         table = funcs[cand[0]]
         agg = defaultdict(lambda: [0, 0, 0])
         tot = [0, 0]
