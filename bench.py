@@ -262,6 +262,33 @@ def run_ours(args, rank, world, local_rank):
     drv.check()
     del stress_logits
 
+    # ---- policy leg: the rollout driven by device policies (SURVEY.md §8f
+    # row 1): tagger / runner MLPs (obs -> 64 -> 64 -> logits) on the tcgen05
+    # tensor cores, sampling fused into their epilogue, then the fused step.
+    # Reported beside `value`, not part of it.
+    policy_leg = None
+    try:
+        pol_t, pol_r = W.Policy.for_tag(cfg, seed=1), W.Policy.for_tag(cfg, seed=2)
+        drv.set_policies(pol_t, pol_r, W.POLICY_BF16)
+        pol_steps = max(1, min(args.steps, 300))
+        for _ in range(3):
+            drv.step()
+        torch.cuda.synchronize()
+        es0.record(stream)
+        for _ in range(pol_steps):
+            drv.step()
+        es1.record(stream)
+        torch.cuda.synchronize()
+        pol_ms = es0.elapsed_time(es1)
+        drv.check()
+        policy_leg = {"policy": "2 x MLP obs->64->64->5 (tagger, runner), bf16 tcgen05, f32 accumulate",
+                      "steps": pol_steps, "env_steps_per_s": E * pol_steps / (pol_ms / 1e3),
+                      "ms_per_step": pol_ms / pol_steps, "gpu_launches_per_step": 3}
+    except Exception as exc:  # reported, never required
+        policy_leg = {"error": str(exc)}
+    finally:
+        drv.set_policies(None, None)
+
     # ---- e2e through the C-ABI host-buffer entry point ----
     n_logits = E * A * Cc * V
     host_logits = torch.zeros(n_logits, dtype=torch.float64).pin_memory()
@@ -315,6 +342,7 @@ def run_ours(args, rank, world, local_rank):
             "sampler_stress": {"logits": "N(0, 3^2), seed 1234", "steps": stress_steps,
                                "env_steps_per_s": E * stress_steps / (stress_ms / 1e3),
                                "ms_per_step": stress_ms / stress_steps},
+            "policy_rollout": policy_leg,
             "gpu_launches": launches,
             "episode_stats": {"episodes": stats[0], "tag_events": stats[3], "env_steps": stats[4]},
             "clocks": clocks.summary(),

@@ -1032,6 +1032,23 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     if (!l0) return;
   }
 
+  // Per-env scalars are loaded first (by the env's lane 0) so their latency
+  // overlaps the per-agent loads instead of following them; packed-env CTAs
+  // (small A, launch/latency-bound) also prefetch their tracker slots.
+  int32_t pre_step = 0, pre_episode = 0;
+  double pre_es[4] = {0.0, 0.0, 0.0, 0.0};  // env_stats [0], [1], [5], [6]
+  if (live && lt == 0) {
+    pre_step = mode == kModeReinit ? 0 : g.step_count[e];
+    pre_episode = (L.episode != nullptr && !(mode == kModeReinit && L.init_episode)) ? L.episode[e] : 0;
+    if (!GRID && mode == kModeFused && L.track) {
+      const double* es = L.env_stats + e * 8;
+      pre_es[0] = es[0];
+      pre_es[1] = es[1];
+      pre_es[2] = es[5];
+      pre_es[3] = es[6];
+    }
+  }
+
   EnvScalars* scal = reinterpret_cast<EnvScalars*>(smem);
   int* scratch = reinterpret_cast<int*>(smem + p.envs_per_cta * sizeof(EnvScalars));
   const EnvSmem s = carve(smem + p.head_bytes + (env_ok ? le : 0) * p.env_bytes, p);
@@ -1222,28 +1239,63 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     }
   }
   if (live) {
+    // Per-agent layout (A % 4 != 0 or packed envs): phases 0+1 fused per
+    // thread like the vec4 path — the agent's state and its logits row (or
+    // action) load together, then sample + apply_move in registers and one
+    // store of the moved state to shared memory (no barrier in between: a
+    // thread only touches its own agents).
+    uint64_t h_env = 0;
+    if (!vec4 && mode != kModeReinit && sample_here) {
+      const uint64_t h_step =
+          L.step_dev != nullptr
+              ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
+              : L.action_h_step;
+      h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
+    }
     for (int a = vec4 ? A : lt; a < A; a += tpe) {
       if (mode != kModeReinit) {
-        const float x = g.loc_x[ga + a], y = g.loc_y[ga + a];
-        s.x[a] = x;
-        s.y[a] = y;
+        float x = g.loc_x[ga + a], y = g.loc_y[ga + a];
+        const uint8_t act = g.active[ga + a];
+        float sp = 0.f, dir = 0.f;
+        if (CONT) {
+          sp = g.speed[ga + a];
+          dir = g.direction[ga + a];
+        }
         integral &= (x == truncf(x)) && (y == truncf(y)) && x >= 0.0f && y >= 0.0f &&
                     x <= p.world_hi && y <= p.world_hi;
-        s.act[a] = g.active[ga + a];
+        const int64_t row = (ga + a) * kC;
+        int32_t act0, act1 = 1;
+        if (sample_here) {
+          const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
+          act0 = sample_tag_row<kV>(L.logits, row, to_unit(absorb(absorb(h_ag, 0), 0)), nonfinite);
+          g.actions[row] = act0;
+          if (CONT) {
+            act1 = sample_tag_row<kV>(L.logits, row + 1, to_unit(absorb(absorb(h_ag, 1), 0)), nonfinite);
+            g.actions[row + 1] = act1;
+          }
+        } else {
+          act0 = g.actions[row];
+          if (CONT) act1 = g.actions[row + 1];
+        }
+        if (act) move_regs<CONT>(p, a, act0, act1, x, y, sp, dir);
+        s.x[a] = x;
+        s.y[a] = y;
+        s.act[a] = act;
         if (CONT) {
-          s.sp[a] = g.speed[ga + a];
-          s.dir[a] = g.direction[ga + a];
+          s.sp[a] = sp;
+          s.dir[a] = dir;
         }
       }
       s.tag[a] = g.is_tagger[ga + a];
       s.cred[a] = 0;
       s.tagged[a] = 0;
     }
+    if (!vec4 && nonfinite && L.error) atomicOr(L.error, kErrNonFinite);
     if (lt == 0) {
       sc.runners_left = 0;
-      sc.step_count = mode == kModeReinit ? 0 : g.step_count[e];
+      sc.step_count = pre_step;
       sc.done = 0;
-      sc.episode = (L.episode != nullptr && !(mode == kModeReinit && L.init_episode)) ? L.episode[e] : 0;
+      sc.episode = pre_episode;
       sc.tags = 0;
       sc.live = 1;
       sc.lattice_ok = 1;
@@ -1259,64 +1311,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
 
   bool reset_now = false;
   if (mode != kModeReinit) {
-    // Phase 1: sample (fused) + move (apply_move, tag_env.cpp:148-160) for
-    // the per-agent (non-vec4) layout; the vec4 layout did both above.
-    if (live && !vec4) {
-      const uint64_t h_step =
-          L.step_dev != nullptr
-              ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
-              : L.action_h_step;
-      const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
-      for (int a = lt; a < A; a += tpe) {
-        int32_t act0, act1 = 1;
-        const int64_t row = (ga + a) * kC;
-        if (sample_here) {
-          const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
-          const double u0 = to_unit(absorb(absorb(h_ag, 0), 0));
-          act0 = sample_tag_row<kV>(L.logits, row, u0, nonfinite);
-          g.actions[row] = act0;
-          if (CONT) {
-            const double u1 = to_unit(absorb(absorb(h_ag, 1), 0));
-            act1 = sample_tag_row<kV>(L.logits, row + 1, u1, nonfinite);
-            g.actions[row + 1] = act1;
-          }
-        } else {
-          act0 = g.actions[row];
-          if (CONT) act1 = g.actions[row + 1];
-        }
-        if (!s.act[a]) continue;
-        if (!CONT) {  // move_discrete, tag_env.hpp:71-82
-          float x = s.x[a], y = s.y[a];
-          switch (act0) {
-            case 1: y = __fadd_rn(y, 1.0f); break;
-            case 2: y = __fsub_rn(y, 1.0f); break;
-            case 3: x = __fsub_rn(x, 1.0f); break;
-            case 4: x = __fadd_rn(x, 1.0f); break;
-            default: break;
-          }
-          s.x[a] = min_ref(max_ref(x, 0.0f), p.world_hi);
-          s.y[a] = min_ref(max_ref(y, 0.0f), p.world_hi);
-        } else {  // move_continuous, tag_env.hpp:86-100
-          float dir = s.dir[a], sp = s.sp[a];
-          if (act1 == 0) dir = __fsub_rn(dir, p.turn_delta);
-          if (act1 == 2) dir = __fadd_rn(dir, p.turn_delta);
-          while (dir >= kTwoPiF) dir = __fsub_rn(dir, kTwoPiF);
-          while (dir < 0.0f) dir = __fadd_rn(dir, kTwoPiF);
-          if (act0 == 0) sp = __fsub_rn(sp, p.accel_delta);
-          if (act0 == 2) sp = __fadd_rn(sp, p.accel_delta);
-          const float ms = a < p.T ? p.max_speed_tagger : p.max_speed_runner;
-          sp = min_ref(max_ref(sp, 0.0f), ms);
-          float x = __fadd_rn(s.x[a], __fmul_rn(sp, cos_ref(dir)));
-          float y = __fadd_rn(s.y[a], __fmul_rn(sp, sin_ref(dir)));
-          s.x[a] = min_ref(max_ref(x, 0.0f), p.world_hi);
-          s.y[a] = min_ref(max_ref(y, 0.0f), p.world_hi);
-          s.dir[a] = dir;
-          s.sp[a] = sp;
-        }
-      }
-      if (nonfinite && L.error) atomicOr(L.error, kErrNonFinite);
-    }
-    if (!vec4) __syncthreads();  // vec4: moved in phase 0, before its barrier
+    // Phase 1 (sample + apply_move, tag_env.cpp:148-160) ran per thread,
+    // fused into phase 0, in both layouts.
 
     // Phase 2: bucket grid over post-move positions (NeighborGrid::build).
     // lattice cells are exact positions: lowest-index tagger per cell
@@ -1399,12 +1395,14 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     }
     if (live) {
       for (int a = vec4 ? A : lt; a < A; a += tpe) {
-        const float r = s.tag[a] ? __fmul_rn(p.reward_per_tag, static_cast<float>(s.cred[a]))
+        const int32_t cr = s.cred[a];
+        const float r = s.tag[a] ? __fmul_rn(p.reward_per_tag, static_cast<float>(cr))
                                  : (s.tagged[a] ? p.penalty : 0.0f);
         if (a < p.T) rt += static_cast<double>(r); else rr += static_cast<double>(r);
         g.rewards[ga + a] = reset_now ? 0.0f : r;
-        g.credits[ga + a] = reset_now ? 0 : s.cred[a];
+        g.credits[ga + a] = reset_now ? 0 : cr;
         g.tagged[ga + a] = reset_now ? 0 : s.tagged[a];
+        if (!single) s.cred[a] = __float_as_int(r);  // summed by the env's lane 0 below
       }
     }
     if (track) {
@@ -1417,9 +1415,6 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           slots[kSlotT + warp] = rt;
           slots[kSlotR + warp] = rr;
         }
-      } else if (live) {
-        atomicAdd(&sc.ret_tagger, rt);
-        atomicAdd(&sc.ret_runner, rr);
       }
     }
     // Single-env CTA that does not reset: its observation inputs are final
@@ -1439,21 +1434,24 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     if (live && lt == 0 && track) {
       // EpisodeTracker::accumulate / finish_done (trainer.cpp:229-252); per-env
       // slots, no atomics: [run_t, run_r, episodes, ret_t, ret_r, tags, steps].
-      double st = sc.ret_tagger, sr = sc.ret_runner;
+      double st = 0.0, sr = 0.0;
       if (single) {
         const double* slots = reinterpret_cast<const double*>(scratch);
-        st = 0.0;
-        sr = 0.0;
         for (int w = 0; w < (blockDim.x >> 5); ++w) {
           st += slots[kSlotT + w];
           sr += slots[kSlotR + w];
         }
+      } else {  // packed env: its A rewards, in agent order
+        for (int a = 0; a < A; ++a) {
+          const double r = static_cast<double>(__int_as_float(s.cred[a]));
+          if (a < p.T) st += r; else sr += r;
+        }
       }
       double* es = L.env_stats + e * 8;
-      const double run_t = es[0] + st;
-      const double run_r = es[1] + sr;
-      es[5] += sc.tags;
-      es[6] += 1.0;
+      const double run_t = (GRID ? es[0] : pre_es[0]) + st;
+      const double run_r = (GRID ? es[1] : pre_es[1]) + sr;
+      es[5] = (GRID ? es[5] : pre_es[2]) + sc.tags;
+      es[6] = (GRID ? es[6] : pre_es[3]) + 1.0;
       if (sc.done) {
         es[2] += 1.0;
         es[3] += run_t;

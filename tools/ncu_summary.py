@@ -36,6 +36,9 @@ KEYS = [
 ]
 
 
+KERNEL = "tag_env_kernel"
+
+
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -48,7 +51,7 @@ def raw(rep):
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             if k in d and units.get(k) in scale:
                 d[k] = str(float(d[k].replace(",", "")) * scale[units[k]])
-        if "tag_env_kernel" in d.get("Kernel Name", ""):
+        if KERNEL in d.get("Kernel Name", ""):
             kernels.append(d)
     return kernels
 
@@ -61,7 +64,10 @@ def num(v):
 
 
 def main():
+    global KERNEL
     rep, tag = sys.argv[1], sys.argv[2]
+    if "--kernel" in sys.argv:
+        KERNEL = sys.argv[sys.argv.index("--kernel") + 1]
     cfg = "c2_fused"
     if "--config" in sys.argv:
         cfg = sys.argv[sys.argv.index("--config") + 1]
@@ -70,7 +76,7 @@ def main():
         algo = float(sys.argv[sys.argv.index("--bytes-per-launch") + 1])
     ks = raw(rep)
     if not ks:
-        sys.exit("no tag_env_kernel in report")
+        sys.exit(f"no {KERNEL} in report")
     d = ks[0]
     lines = [f"# ncu summary `{tag}`", "", f"kernel: `{d.get('Kernel Name')}`", "",
              f"report: `{os.path.basename(rep)}` (`ncu --set full --clock-control none`, 1 launch, "
