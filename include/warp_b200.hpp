@@ -235,6 +235,51 @@ class ResetManager {
   wdg_resets* h_ = nullptr;
 };
 
+// PolicyParams + init_policy / forward (proj/include/warp/policy_model.hpp)
+// with device-resident parameters.
+enum class PolicyPrecision : int32_t { F64 = WDG_POLICY_F64, BF16 = WDG_POLICY_BF16 };
+struct PolicyDims {  // policy_model.hpp:20-28
+  int64_t obs_dim = 0;
+  std::vector<int64_t> hidden = {64, 64};
+  int64_t num_categories = 1;
+  int64_t num_choices = 1;
+};
+class Policy {
+ public:
+  explicit Policy(const PolicyDims& d) {
+    check(wdg_policy_create(d.obs_dim, d.hidden.data(), static_cast<int32_t>(d.hidden.size()),
+                            d.num_categories, d.num_choices, &h_));
+  }
+  Policy(const PolicyDims& d, uint64_t seed) : Policy(d) { init(seed); }
+  ~Policy() { wdg_policy_destroy(h_); }
+  Policy(const Policy&) = delete;
+  Policy& operator=(const Policy&) = delete;
+  void init(uint64_t seed) { check(wdg_policy_init(h_, seed)); }  // init_policy
+  int64_t param_count() const {
+    int64_t n = 0;
+    check(wdg_policy_param_count(h_, &n));
+    return n;
+  }
+  // for_each_param canonical order (policy_model.hpp:43-46)
+  std::vector<double> params() const {
+    std::vector<double> v(static_cast<size_t>(param_count()));
+    check(wdg_policy_get_params(h_, v.data(), static_cast<int64_t>(v.size())));
+    return v;
+  }
+  void set_params(const std::vector<double>& v) {
+    check(wdg_policy_set_params(h_, v.data(), static_cast<int64_t>(v.size())));
+  }
+  // forward over agents [a0, a1) of device obs [E, A, obs_dim] -> device logits / values
+  void forward(const float* obs, int64_t E, int64_t A, int64_t a0, int64_t a1, double* logits,
+               double* values, PolicyPrecision prec = PolicyPrecision::F64, void* stream = nullptr) const {
+    check(wdg_policy_forward(h_, obs, E, A, a0, a1, logits, values, static_cast<int32_t>(prec), stream));
+  }
+  const wdg_policy* raw() const { return h_; }
+
+ private:
+  wdg_policy* h_ = nullptr;
+};
+
 // RolloutDriver (harness.cpp:428-505): fused sample -> step -> reset launch.
 class RolloutDriver {
  public:
@@ -247,6 +292,13 @@ class RolloutDriver {
   RolloutDriver& operator=(const RolloutDriver&) = delete;
   void set_logits(const double* device_logits, int64_t count) {
     check(wdg_rollout_set_logits(h_, device_logits, count));
+  }
+  // RolloutDriver(ws, &map, &policies, seed) (harness.cpp:428-476): the
+  // tagger / runner policies run on device before every step.
+  void set_policies(const Policy* tagger, const Policy* runner,
+                    PolicyPrecision prec = PolicyPrecision::F64) {
+    check(wdg_rollout_set_policies(h_, tagger ? tagger->raw() : nullptr, runner ? runner->raw() : nullptr,
+                                   static_cast<int32_t>(prec)));
   }
   void step() { check(wdg_rollout_step(h_)); }
   void step_host(const double* host_logits, int64_t count, float* host_rewards, uint8_t* host_done) {

@@ -26,7 +26,18 @@ int main() {
     const std::vector<float> obs = store.pull<float>(kObservations, 0, 1);
     std::printf("episodes=%.0f tag_events=%.0f env_steps=%.0f obs[0]=%g\n", st[WDG_STAT_EPISODES],
                 st[WDG_STAT_TAG_EVENTS], st[WDG_STAT_ENV_STEPS], obs[0]);
-    return st[WDG_STAT_ENV_STEPS] == 16 * 40 ? 0 : 1;
+    // The same driver stepped by device policies (RolloutDriver with
+    // tag_policy_map, harness.cpp:395-399,428-476).
+    PolicyDims d;
+    d.obs_dim = 4 * cfg.k_nearest + 3;
+    d.num_choices = 5;
+    Policy tagger(d, 1), runner(d, 2);
+    driver.set_policies(&tagger, &runner, PolicyPrecision::BF16);
+    driver.run(10);
+    driver.check_errors();
+    const std::vector<double> st2 = driver.stats();
+    std::printf("policy rollout: env_steps=%.0f\n", st2[WDG_STAT_ENV_STEPS]);
+    return (st[WDG_STAT_ENV_STEPS] == 16 * 40 && st2[WDG_STAT_ENV_STEPS] == 16 * 50) ? 0 : 1;
   } catch (const Error& e) {
     std::fprintf(stderr, "error %d: %s\n", static_cast<int>(e.code()), e.what());
     return 2;
