@@ -75,6 +75,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
@@ -1096,6 +1099,16 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         if (CONT) {
           bulk_g2s(s.sp, g.speed + ga, rowb, bar);
           bulk_g2s(s.dir, g.direction + ga, rowb, bar);
+        }
+        // L2 prefetch of the inputs of the env that will start about one CTA
+        // lifetime from now (the next wave: `prefetch_stride` resident CTAs
+        // later), so its bulk copies hit L2 instead of HBM.
+        const int64_t pe = e + p.prefetch_stride;
+        if (p.prefetch_stride > 0 && pe < p.E) {
+          const int64_t pa = pe * A;
+          if (lgb) bulk_prefetch_l2(L.logits + pa * kC * kV, lgb);
+          bulk_prefetch_l2(g.loc_x + pa, rowb);
+          bulk_prefetch_l2(g.loc_y + pa, rowb);
         }
       }
       __syncthreads();  // barrier initialised before anyone waits on it

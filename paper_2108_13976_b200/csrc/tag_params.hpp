@@ -91,6 +91,7 @@ struct TagDevConfig {
   int32_t head_bytes = 0;         // CTA header (per-env scalars + scan scratch + mbarrier)
   int32_t bulk_in = 0;            // fused/step inputs staged by TMA bulk copies (one env per CTA)
   int32_t off_zone = 0;           // CTA offset of the bulk logits landing zone
+  int32_t prefetch_stride = 0;    // bulk path: L2-prefetch env e + stride's inputs (0 = off)
   int32_t smem_bytes = 0;         // total dynamic smem per CTA
 };
 
