@@ -312,6 +312,38 @@ WDG_API wdg_status wdg_rollout_set_keep_policy_outputs(wdg_rollout* rollout, int
 WDG_API wdg_status wdg_rollout_policy_outputs(wdg_rollout* rollout, const double** logits,
                                               const double** values);
 
+/* ---- Rollout capture + returns (proj/include/warp/trainer.hpp:36-53) ---- */
+/* RolloutBatch in HBM: obs [T,E,A,D] f32, actions [T,E,A,C] i32, rewards
+ * [T,E,A] f32, done [T,E] u8, active [T,E,A] u8, values / logp [T,E,A] f64,
+ * bootstrap [E,A] f64 — the reference layout (trainer.hpp:36-49). */
+typedef struct wdg_batch wdg_batch;
+typedef struct wdg_batch_view {
+  int64_t horizon, num_envs, num_agents, obs_dim, num_categories;
+  float* obs;
+  int32_t* actions;
+  float* rewards;
+  uint8_t* done;
+  uint8_t* active;
+  double* values;
+  double* logp;
+  double* bootstrap;
+} wdg_batch_view;
+/* RolloutBatch::resize(T, E, A, D, C) (trainer.cpp:58-71), dims taken from the
+ * store's observations / sampled_actions arrays. */
+WDG_API wdg_status wdg_batch_create(const wdg_store* store, int64_t horizon, wdg_batch** out);
+WDG_API void wdg_batch_destroy(wdg_batch* batch);
+WDG_API wdg_status wdg_batch_get_view(const wdg_batch* batch, wdg_batch_view* out);
+/* Trainer::collect (trainer.cpp:315-403) on device: `horizon` policy-driven
+ * rollout steps (wdg_rollout_set_policies first) captured into the batch —
+ * pre-step obs and values, sampled actions, active flags and log-prob at
+ * sample time, rewards and done before reset-on-done — then the bootstrap
+ * values of the final observations. */
+WDG_API wdg_status wdg_rollout_collect(wdg_rollout* rollout, wdg_batch* batch);
+/* compute_returns(batch, gamma) (trainer.cpp:73-88) into DEVICE f64 returns
+ * [T,E,A]: R_t = r_t + gamma * (1 - done_t) * R_{t+1}, R_T = bootstrap. */
+WDG_API wdg_status wdg_compute_returns(const wdg_batch* batch, double gamma, double* device_returns,
+                                       void* cuda_stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

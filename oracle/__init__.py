@@ -150,6 +150,12 @@ def oracle_lib():
         lib.oracle_policy_forward.argtypes = [C.POINTER(C.c_double), C.c_int64, I64P, C.c_int32, C.c_int64,
                                               C.c_int64, C.POINTER(C.c_float), C.c_int64,
                                               C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.oracle_logp.restype = None
+        lib.oracle_compute_returns.restype = None
+        lib.oracle_logp.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int64, C.c_int64, C.c_int64,
+                                    C.POINTER(C.c_double)]
+        lib.oracle_compute_returns.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_uint8), C.POINTER(C.c_double),
+                                               C.c_int64, C.c_int64, C.c_int64, C.c_double, C.POINTER(C.c_double)]
         _oracle_lib = lib
     return _oracle_lib
 
@@ -197,6 +203,9 @@ def ref_lib():
         lib.ref_policy_forward.argtypes = [C.POINTER(C.c_double), C.c_int64, I64P, C.c_int32, C.c_int64,
                                            C.c_int64, C.POINTER(C.c_float), C.c_int64,
                                            C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.ref_compute_returns.restype = C.c_int
+        lib.ref_compute_returns.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_uint8), C.POINTER(C.c_double),
+                                            C.c_int64, C.c_int64, C.c_int64, C.c_double, C.POINTER(C.c_double)]
         _ref_lib = lib
     return _ref_lib
 
@@ -443,3 +452,80 @@ def tag_policy_logits(world, cfg, params_tagger, params_runner, dims: PolicyDims
         logits[:, :T] = lt.reshape(E, T, W)
         logits[:, T:] = lr.reshape(E, A - T, W)
     return logits.reshape(-1)
+
+
+def tag_policy_forward(world, cfg, params_tagger, params_runner, dims: PolicyDims, ref: bool = False):
+    """(logits [E*A*C*V], values [E*A]) of forward_policies on a world's obs."""
+    E = world.num_envs
+    A = cfg.num_taggers + cfg.num_runners
+    T = cfg.num_taggers
+    obs = world.pull("observations").reshape(E, A, dims.obs_dim)
+    W = dims.logits_width()
+    logits = np.zeros((E, A, W), dtype=np.float64)
+    values = np.zeros((E, A), dtype=np.float64)
+    if params_runner is None or params_runner is params_tagger:
+        lg, v = policy_forward(params_tagger, dims, obs.reshape(-1, dims.obs_dim), ref)
+        logits[:], values[:] = lg.reshape(E, A, W), v.reshape(E, A)
+    else:
+        lt, vt = policy_forward(params_tagger, dims, obs[:, :T].reshape(-1, dims.obs_dim), ref)
+        lr, vr = policy_forward(params_runner, dims, obs[:, T:].reshape(-1, dims.obs_dim), ref)
+        logits[:, :T], values[:, :T] = lt.reshape(E, T, W), vt.reshape(E, T)
+        logits[:, T:], values[:, T:] = lr.reshape(E, A - T, W), vr.reshape(E, A - T)
+    return logits.reshape(-1), values.reshape(-1)
+
+
+def logp_of(logits: np.ndarray, actions: np.ndarray, C: int, V: int) -> np.ndarray:
+    """category_stats(...).logp summed over categories (trainer.cpp:386-392)."""
+    rows = actions.size // C
+    lg = np.ascontiguousarray(logits, dtype=np.float64)
+    ac = np.ascontiguousarray(actions, dtype=np.int32)
+    out = np.zeros(rows, dtype=np.float64)
+    oracle_lib().oracle_logp(_dbl_p(lg), ac.ctypes.data_as(C_i32p()), rows, C, V, _dbl_p(out))
+    return out
+
+
+def C_i32p():
+    return C.POINTER(C.c_int32)
+
+
+def compute_returns(rewards, done, bootstrap, gamma: float, ref: bool = False) -> np.ndarray:
+    """compute_returns (trainer.cpp:73-88); rewards [T,E,A], done [T,E], bootstrap [E,A]."""
+    r = np.ascontiguousarray(rewards, dtype=np.float32)
+    d = np.ascontiguousarray(done, dtype=np.uint8)
+    b = np.ascontiguousarray(bootstrap, dtype=np.float64)
+    T, E, A = r.shape
+    out = np.zeros((T, E, A), dtype=np.float64)
+    fn = ref_lib().ref_compute_returns if ref else oracle_lib().oracle_compute_returns
+    st = fn(r.ctypes.data_as(C.POINTER(C.c_float)), d.ctypes.data_as(C.POINTER(C.c_uint8)), _dbl_p(b),
+            T, E, A, float(gamma), _dbl_p(out))
+    if ref and st:
+        raise ValueError(f"compute_returns failed with status {st}")
+    return out
+
+
+def collect(world, cfg, params_tagger, params_runner, dims: PolicyDims, horizon: int, first_step: int,
+            seed: int):
+    """Trainer::collect (trainer.cpp:315-403) on the oracle world: per step
+    the pre-step obs and values, the sampled actions / active flags / logp at
+    sample time, rewards and done before reset; then the bootstrap values."""
+    E = world.num_envs
+    A = cfg.num_taggers + cfg.num_runners
+    Cc, V = dims.num_categories, dims.num_choices
+    out = {k: [] for k in ("obs", "actions", "rewards", "done", "active", "values", "logp")}
+    for t in range(horizon):
+        out["obs"].append(world.pull("observations").copy())
+        logits, values = tag_policy_forward(world, cfg, params_tagger, params_runner, dims)
+        out["values"].append(values.reshape(E, A))
+        world.sample(first_step + t, seed, logits)
+        acts = world.pull("sampled_actions").copy()
+        out["actions"].append(acts)
+        out["active"].append(world.pull("active").copy())
+        out["logp"].append(logp_of(logits, acts, Cc, V).reshape(E, A))
+        world.step(first_step + t)
+        world.track()
+        out["rewards"].append(world.pull("rewards").copy())
+        out["done"].append(world.pull("done").copy())
+        world.reset_done()
+    res = {k: np.stack(v) for k, v in out.items()}
+    res["bootstrap"] = tag_policy_forward(world, cfg, params_tagger, params_runner, dims)[1].reshape(E, A)
+    return res

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "warp/policy_model.hpp"
+#include "warp/trainer.hpp"
 #include "warp/data_store.hpp"
 #include "warp/reset_manager.hpp"
 #include "warp/sampler.hpp"
@@ -342,6 +343,23 @@ __attribute__((visibility("default"))) int ref_policy_forward(const double* para
     warp::forward_parallel(p, x, rows, 1, lg, vals);
     if (logits) std::copy(lg.begin(), lg.end(), logits);
     if (values) std::copy(vals.begin(), vals.end(), values);
+    return 0;
+  });
+}
+
+// compute_returns(batch, gamma) (trainer.cpp:73-88) on a batch filled from
+// the given arrays.
+__attribute__((visibility("default"))) int ref_compute_returns(const float* rewards, const uint8_t* done,
+                                                               const double* bootstrap, int64_t T, int64_t E,
+                                                               int64_t A, double gamma, double* returns) {
+  return guarded([&] {
+    warp::RolloutBatch b;
+    b.resize(T, E, A, 1, 1);
+    std::copy(rewards, rewards + T * E * A, b.rewards.begin());
+    std::copy(done, done + T * E, b.done.begin());
+    std::copy(bootstrap, bootstrap + E * A, b.bootstrap.begin());
+    const std::vector<double> r = warp::compute_returns(b, gamma);
+    std::copy(r.begin(), r.end(), returns);
     return 0;
   });
 }

@@ -657,3 +657,36 @@ int oracle_policy_forward(const double* params, int64_t obs_dim, const int64_t* 
   free(next);
   return 0;
 }
+
+/* ---- rollout batch (proj/src/trainer.cpp) --------------------------------- */
+
+void oracle_logp(const double* logits, const int32_t* actions, int64_t rows, int64_t C, int64_t V,
+                 double* logp) {
+  for (int64_t i = 0; i < rows; ++i) {
+    double lp = 0.0;
+    for (int64_t c = 0; c < C; ++c) {
+      const double* z = logits + (i * C + c) * V;
+      double zmax = z[0];
+      for (int64_t k = 1; k < V; ++k) zmax = zmax < z[k] ? z[k] : zmax;
+      double sum = 0.0;
+      for (int64_t k = 0; k < V; ++k) sum += exp(z[k] - zmax);
+      lp += z[actions[i * C + c]] - zmax - log(sum);
+    }
+    logp[i] = lp;
+  }
+}
+
+void oracle_compute_returns(const float* rewards, const uint8_t* done, const double* bootstrap, int64_t T,
+                            int64_t E, int64_t A, double gamma, double* returns) {
+  for (int64_t e = 0; e < E; ++e) {
+    for (int64_t a = 0; a < A; ++a) {
+      double next = bootstrap[e * A + a];
+      for (int64_t t = T - 1; t >= 0; --t) {
+        const int64_t idx = (t * E + e) * A + a;
+        const double cont = done[t * E + e] ? 0.0 : 1.0;
+        next = (double)rewards[idx] + gamma * cont * next;
+        returns[idx] = next;
+      }
+    }
+  }
+}

@@ -77,6 +77,16 @@ int oracle_policy_forward(const double* params, int64_t obs_dim, const int64_t* 
                           int32_t num_hidden, int64_t num_categories, int64_t num_choices,
                           const float* obs, int64_t rows, double* logits, double* values);
 
+/* ---- rollout batch (proj/src/trainer.cpp) ------------------------------- */
+/* category_stats(z, V, a).logp summed over C categories (trainer.cpp:25-41,
+ * 386-392), per row. */
+void oracle_logp(const double* logits, const int32_t* actions, int64_t rows, int64_t C, int64_t V,
+                 double* logp);
+/* compute_returns (trainer.cpp:73-88): rewards [T,E,A], done [T,E],
+ * bootstrap [E,A] -> returns [T,E,A]. */
+void oracle_compute_returns(const float* rewards, const uint8_t* done, const double* bootstrap, int64_t T,
+                            int64_t E, int64_t A, double gamma, double* returns);
+
 #ifdef __cplusplus
 }
 #endif

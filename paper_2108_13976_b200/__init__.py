@@ -73,6 +73,7 @@ EXPORTED_SYMBOLS = [
     "wdg_policy_create", "wdg_policy_destroy", "wdg_policy_init", "wdg_policy_param_count",
     "wdg_policy_set_params", "wdg_policy_get_params", "wdg_policy_forward", "wdg_rollout_set_policies",
     "wdg_rollout_policy_outputs", "wdg_copy_to_host", "wdg_rollout_set_keep_policy_outputs",
+    "wdg_batch_create", "wdg_batch_destroy", "wdg_batch_get_view", "wdg_rollout_collect", "wdg_compute_returns",
 ]
 
 POLICY_F64, POLICY_BF16 = 0, 1
@@ -95,6 +96,14 @@ class _TagConfigC(C.Structure):
                 ("tag_reward", C.c_double), ("tagged_penalty", C.c_double),
                 ("max_speed_tagger", C.c_double), ("max_speed_runner", C.c_double),
                 ("accel_delta", C.c_double), ("turn_delta", C.c_double), ("seed", C.c_uint64)]
+
+
+class _BatchViewC(C.Structure):
+    _fields_ = [("horizon", C.c_int64), ("num_envs", C.c_int64), ("num_agents", C.c_int64),
+                ("obs_dim", C.c_int64), ("num_categories", C.c_int64), ("obs", C.c_void_p),
+                ("actions", C.c_void_p), ("rewards", C.c_void_p), ("done", C.c_void_p),
+                ("active", C.c_void_p), ("values", C.c_void_p), ("logp", C.c_void_p),
+                ("bootstrap", C.c_void_p)]
 
 
 class _ArrayInfoC(C.Structure):
@@ -186,6 +195,11 @@ def _load():
         "wdg_rollout_policy_outputs": (I32, [P, C.POINTER(P), C.POINTER(P)]),
         "wdg_copy_to_host": (I32, [P, P, I64]),
         "wdg_rollout_set_keep_policy_outputs": (I32, [P, I32]),
+        "wdg_batch_create": (I32, [P, I64, C.POINTER(P)]),
+        "wdg_batch_destroy": (None, [P]),
+        "wdg_batch_get_view": (I32, [P, C.POINTER(_BatchViewC)]),
+        "wdg_rollout_collect": (I32, [P, P]),
+        "wdg_compute_returns": (I32, [P, D, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -600,6 +614,10 @@ class RolloutDriver:
         _check(self._lib.wdg_rollout_policy_outputs(self._h, C.byref(lg), C.byref(vl)))
         return lg.value or 0, vl.value or 0
 
+    def collect(self, batch: "RolloutBatch"):
+        """Trainer::collect (trainer.cpp:315-403): horizon captured policy steps."""
+        _check(self._lib.wdg_rollout_collect(self._h, batch._h))
+
     def set_fused(self, fused: bool):
         _check(self._lib.wdg_rollout_set_fused(self._h, 1 if fused else 0))
 
@@ -706,6 +724,48 @@ class Policy:
         _check(self._lib.wdg_policy_forward(self._h, C.c_void_p(_ptr(obs)), num_envs, num_agents, agent_begin,
                                             end, C.c_void_p(_ptr(logits)), C.c_void_p(_ptr(values)),
                                             precision, st))
+
+
+class RolloutBatch:
+    """RolloutBatch (trainer.hpp:36-49) in HBM, filled by RolloutDriver.collect."""
+
+    FIELDS = {"obs": np.float32, "actions": np.int32, "rewards": np.float32, "done": np.uint8,
+              "active": np.uint8, "values": np.float64, "logp": np.float64, "bootstrap": np.float64}
+
+    def __init__(self, store: DataStore, horizon: int):
+        self._lib = _load()
+        h = C.c_void_p()
+        _check(self._lib.wdg_batch_create(store._h, int(horizon), C.byref(h)))
+        self._h = h
+        v = _BatchViewC()
+        _check(self._lib.wdg_batch_get_view(self._h, C.byref(v)))
+        self.view = v
+        T, E, A, D, Cc = v.horizon, v.num_envs, v.num_agents, v.obs_dim, v.num_categories
+        self.shapes = {"obs": (T, E, A, D), "actions": (T, E, A, Cc), "rewards": (T, E, A), "done": (T, E),
+                       "active": (T, E, A), "values": (T, E, A), "logp": (T, E, A), "bootstrap": (E, A)}
+        store._deps.append(self)
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wdg_batch_destroy(self._h)
+            self._h = None
+
+    def device_ptr(self, name: str) -> int:
+        return getattr(self.view, name)
+
+    def pull(self, name: str) -> np.ndarray:
+        out = np.zeros(self.shapes[name], dtype=self.FIELDS[name])
+        return copy_to_host(self.device_ptr(name), out)
+
+    def compute_returns(self, gamma: float, out=None, stream=None):
+        """compute_returns (trainer.cpp:73-88) into a device f64 [T,E,A] buffer
+        (a torch tensor or address); returns it."""
+        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        _check(self._lib.wdg_compute_returns(self._h, float(gamma), C.c_void_p(_ptr(out)), st))
+        return out
 
 
 class Workspace:

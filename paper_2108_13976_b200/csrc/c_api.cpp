@@ -8,6 +8,7 @@
 
 #include "facade.hpp"
 #include "policy.hpp"
+#include "batch.hpp"
 
 struct wdg_store {
   std::unique_ptr<wdg::DataStore> impl;
@@ -23,6 +24,9 @@ struct wdg_rollout {
 };
 struct wdg_policy {
   std::unique_ptr<wdg::Policy> impl;
+};
+struct wdg_batch {
+  std::unique_ptr<wdg::RolloutBatch> impl;
 };
 
 namespace {
@@ -497,6 +501,42 @@ wdg_status wdg_copy_to_host(const void* device_src, void* host_dst, int64_t byte
     need(host_dst, "host_dst");
     wdg::cuda_check(cudaMemcpy(host_dst, device_src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost),
                     "copy_to_host");
+  });
+}
+
+wdg_status wdg_batch_create(const wdg_store* store, int64_t horizon, wdg_batch** out) {
+  return guarded([&] {
+    need(out, "out");
+    const wdg::DataStore& st = *need(store, "store")->impl;
+    const wdg::ArrayInfo& obs = st.info(st.handle(wdg::kObservations));
+    const wdg::ArrayInfo& act = st.info(st.handle(wdg::kSampledActions));
+    auto b = std::make_unique<wdg_batch>();
+    b->impl = std::make_unique<wdg::RolloutBatch>(horizon, st.num_envs(), st.num_agents(), obs.agent_stride,
+                                                  act.agent_stride);
+    *out = b.release();
+  });
+}
+
+void wdg_batch_destroy(wdg_batch* batch) { delete batch; }
+
+wdg_status wdg_batch_get_view(const wdg_batch* batch, wdg_batch_view* out) {
+  return guarded([&] {
+    const wdg::RolloutBatch& b = *need(batch, "batch")->impl;
+    need(out, "out");
+    *out = wdg_batch_view{b.T, b.E, b.A, b.D, b.C, b.obs, b.actions, b.rewards, b.done,
+                          b.active, b.values, b.logp, b.bootstrap};
+  });
+}
+
+wdg_status wdg_rollout_collect(wdg_rollout* rollout, wdg_batch* batch) {
+  return guarded([&] { need(rollout, "rollout")->impl->collect(*need(batch, "batch")->impl); });
+}
+
+wdg_status wdg_compute_returns(const wdg_batch* batch, double gamma, double* device_returns, void* cuda_stream) {
+  return guarded([&] {
+    wdg::compute_returns(*need(batch, "batch")->impl, gamma, device_returns,
+                         static_cast<cudaStream_t>(cuda_stream));
+    wdg::cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(cuda_stream)), "compute_returns");
   });
 }
 

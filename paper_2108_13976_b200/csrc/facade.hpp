@@ -195,6 +195,7 @@ class ResetManager {
 };
 
 class Policy;
+class RolloutBatch;
 
 // RolloutDriver (harness.cpp:428-505).
 class Rollout {
@@ -218,6 +219,8 @@ class Rollout {
   void set_fused(bool f) { fused_ = f; }
   void set_graphs(bool g) { graphs_ = g; }
   void step();
+  // Trainer::collect (trainer.cpp:315-403): T captured policy steps.
+  void collect(RolloutBatch& batch);
   void step_host(const double* host_logits, int64_t count, float* host_rewards, uint8_t* host_done);
   void run(int64_t steps);
   void reduce_stats_into(double* device_out);
@@ -230,7 +233,8 @@ class Rollout {
  private:
   TagLaunch fused_launch(int64_t step) const;
   void step_unfused();
-  void forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add);
+  void forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add,
+                        double* values_out, bool force_logits, bool sample);
   bool policy_samples() const { return pol_[0] != nullptr && pol_prec_ == 1; }  // kPolicyBF16
   const Policy* pol_[2] = {nullptr, nullptr};
   int32_t pol_prec_ = 0;

@@ -9,6 +9,7 @@
 
 #include "facade.hpp"
 #include "policy.hpp"
+#include "batch.hpp"
 #include "kernels.hpp"
 
 namespace wdg {
@@ -629,14 +630,16 @@ void Rollout::set_policies(const Policy* tagger, const Policy* runner, int32_t p
 // forward_policies (harness.cpp:445-476): obs (already in HBM) -> f64 logits,
 // or (bf16) the tensor-core forward fused with sample_actions for step t ->
 // sampled actions, which the fused env launch then reads (L.logits == nullptr).
-void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add) {
+// values_out / force_logits / sample serve the rollout capture (collect).
+void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add,
+                               double* values_out, bool force_logits, bool sample) {
   if (pol_[0] == nullptr) return;
   const TagDevConfig& p = plan_.dev();
   const float* obs = static_cast<const float*>(store_.device_ptr(store_.handle(kObservations)));
   // f64 logits are the sampler's input (always written); bf16 samples in the
   // epilogue and stores logits / values only when asked to keep them.
-  double* lg = (pol_prec_ == kPolicyBF16 && !keep_outputs_) ? nullptr : pol_logits_;
-  double* vl = keep_outputs_ ? pol_values_ : nullptr;
+  double* lg = (pol_prec_ == kPolicyBF16 && !keep_outputs_ && !force_logits) ? nullptr : pol_logits_;
+  double* vl = values_out ? values_out : (keep_outputs_ ? pol_values_ : nullptr);
   if (pol_prec_ == kPolicyBF16) {
     SampleKeys k;
     k.env_offset = p.env_offset;
@@ -644,7 +647,7 @@ void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* ste
     k.step_dev = step_dev;
     k.step_add = step_add;
     k.h0 = h_actions0_;
-    int32_t* act = static_cast<int32_t*>(store_.device_ptr(store_.handle(kSampledActions)));
+    int32_t* act = sample ? static_cast<int32_t*>(store_.device_ptr(store_.handle(kSampledActions))) : nullptr;
     if (pol_[0] == pol_[1]) {
       pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.A, act, lg, vl, k, st, error_);
     } else {
@@ -661,6 +664,39 @@ void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* ste
   }
 }
 
+// Trainer::collect (trainer.cpp:315-403) on device: T steps of the policy
+// rollout, each captured into slot t of the batch —
+//   policy_forward(t): obs before the step, values of the forward;
+//   sample(t):         sampled actions, active flags at sample time, logp;
+//   post_step(t):      rewards and done of the step (before reset-on-done);
+// then the bootstrap values of the final observations.
+void Rollout::collect(RolloutBatch& b) {
+  const TagDevConfig& p = plan_.dev();
+  if (pol_[0] == nullptr) raise(Errc::state_error, "collect: set the policies first (Trainer::collect runs them)");
+  if (!fused_ok()) raise(Errc::state_error, "collect: needs the fused step with the Tag reset policy");
+  if (b.E != p.E || b.A != p.A || b.D != p.D || b.C != p.C) {
+    raise(Errc::shape_mismatch, "collect: batch dims do not match the store / Tag config");
+  }
+  cudaStream_t st = store_.stream();
+  const float* obs = static_cast<const float*>(store_.device_ptr(store_.handle(kObservations)));
+  const int64_t EA = int64_t{p.E} * p.A;
+  for (int64_t t = 0; t < b.T; ++t) {
+    cuda_check(cudaMemcpyAsync(b.obs + t * EA * p.D, obs, static_cast<size_t>(EA * p.D) * sizeof(float),
+                               cudaMemcpyDeviceToDevice, st),
+               "collect obs");
+    forward_policies(st, t_, nullptr, 0, b.values + t * EA, true, true);
+    TagLaunch L = fused_launch(t_);
+    L.cap_actions = b.actions + t * EA * p.C;
+    L.cap_active = b.active + t * EA;
+    L.cap_rewards = b.rewards + t * EA;
+    L.cap_done = b.done + t * p.E;
+    plan_.launch(L);
+    launch_logp(pol_logits_, b.actions + t * EA * p.C, b.logp + t * EA, EA, p.C, p.V, st);
+    ++t_;
+  }
+  forward_policies(st, t_, nullptr, 0, b.bootstrap, true, false);
+}
+
 void Rollout::step_unfused() {
   const TagDevConfig& p = plan_.dev();
   const uint64_t h_step = host_absorb(h_actions0_, static_cast<uint64_t>(t_));
@@ -674,7 +710,7 @@ void Rollout::step_unfused() {
 }
 
 void Rollout::step() {
-  forward_policies(store_.stream(), t_, nullptr, 0);
+  forward_policies(store_.stream(), t_, nullptr, 0, nullptr, false, true);
   if (fused_ok()) {
     plan_.launch(fused_launch(t_));
   } else {
@@ -758,7 +794,7 @@ void Rollout::build_graph() {
   for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
     if (pol_[0] != nullptr) {
       try {
-        forward_policies(cap, 0, step_dev_, i);
+        forward_policies(cap, 0, step_dev_, i, nullptr, false, true);
       } catch (const Error&) {
         err = cudaErrorUnknown;
         break;

@@ -1206,6 +1206,16 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           *reinterpret_cast<int4*>(g.actions + ga + a0) = make_int4(act0[0], act0[1], act0[2], act0[3]);
         }
       }
+      if (L.cap_actions != nullptr) {
+        if (CONT) {
+          int4* dst = reinterpret_cast<int4*>(L.cap_actions + (ga + a0) * 2);
+          dst[0] = make_int4(act0[0], act1[0], act0[1], act1[1]);
+          dst[1] = make_int4(act0[2], act1[2], act0[3], act1[3]);
+        } else {
+          *reinterpret_cast<int4*>(L.cap_actions + ga + a0) = make_int4(act0[0], act0[1], act0[2], act0[3]);
+        }
+        *reinterpret_cast<uint32_t*>(L.cap_active + ga + a0) = act4;
+      }
       float xs[4] = {x4.x, x4.y, x4.z, x4.w}, ys[4] = {y4.x, y4.y, y4.z, y4.w};
       float sps[4] = {sp4.x, sp4.y, sp4.z, sp4.w}, dirs[4] = {dir4.x, dir4.y, dir4.z, dir4.w};
 #pragma unroll
@@ -1289,6 +1299,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         } else {
           act0 = g.actions[row];
           if (CONT) act1 = g.actions[row + 1];
+        }
+        if (L.cap_actions != nullptr) {
+          L.cap_actions[row] = act0;
+          if (CONT) L.cap_actions[row + 1] = act1;
+          L.cap_active[ga + a] = act;
         }
         if (act) move_regs<CONT>(p, a, act0, act1, x, y, sp, dir);
         s.x[a] = x;
@@ -1379,6 +1394,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
 
     // Phase 4: rewards (write_rewards_row, tag_env.cpp:252-259) + tracker.
     reset_now = live && mode == kModeFused && L.do_reset && done_now;
+    if (L.cap_done != nullptr && live && lt == 0) L.cap_done[e] = done_now ? 1 : 0;
     const bool track = mode == kModeFused && L.track;
     double rt = 0.0, rr = 0.0;
     if (live && vec4) {
@@ -1395,6 +1411,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           r[k] = is_t ? __fmul_rn(p.reward_per_tag, static_cast<float>(cr[k])) : (was ? p.penalty : 0.0f);
           if (a0 + k < p.T) rt += static_cast<double>(r[k]); else rr += static_cast<double>(r[k]);
         }
+        if (L.cap_rewards != nullptr)
+          *reinterpret_cast<float4*>(L.cap_rewards + ga + a0) = make_float4(r[0], r[1], r[2], r[3]);
         if (reset_now) {
           *reinterpret_cast<float4*>(g.rewards + ga + a0) = make_float4(0.f, 0.f, 0.f, 0.f);
           *reinterpret_cast<int4*>(g.credits + ga + a0) = make_int4(0, 0, 0, 0);
@@ -1413,6 +1431,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
                                  : (s.tagged[a] ? p.penalty : 0.0f);
         if (a < p.T) rt += static_cast<double>(r); else rr += static_cast<double>(r);
         g.rewards[ga + a] = reset_now ? 0.0f : r;
+        if (L.cap_rewards != nullptr) L.cap_rewards[ga + a] = r;
         g.credits[ga + a] = reset_now ? 0 : cr;
         g.tagged[ga + a] = reset_now ? 0 : s.tagged[a];
         if (!single) s.cred[a] = __float_as_int(r);  // summed by the env's lane 0 below

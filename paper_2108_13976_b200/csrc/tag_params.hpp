@@ -115,6 +115,14 @@ struct TagLaunch {
   // tagger_return, runner_return, tag_events, env_steps, (pad).
   double* env_stats = nullptr;
   uint32_t* error = nullptr;          // sticky error word
+  // Rollout capture (Trainer::collect hooks, trainer.cpp:357-397), fused into
+  // the step: the sampled actions and the active flags at sample time, and
+  // the step's rewards and done BEFORE reset-on-done, into caller slots
+  // ([E, A, C], [E, A], [E, A], [E]); nullptr = no capture.
+  int32_t* cap_actions = nullptr;
+  uint8_t* cap_active = nullptr;
+  float* cap_rewards = nullptr;
+  uint8_t* cap_done = nullptr;
   // Performance-analysis only (WDG_ABLATE env var, never set by the product,
   // tests or bench): bit0 skip exp/sampling, bit1 skip cell K-NN, bit2 skip
   // obs rows, bit3 skip grid build. Results are WRONG when non-zero.
