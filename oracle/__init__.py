@@ -150,6 +150,12 @@ def oracle_lib():
         lib.oracle_policy_forward.argtypes = [C.POINTER(C.c_double), C.c_int64, I64P, C.c_int32, C.c_int64,
                                               C.c_int64, C.POINTER(C.c_float), C.c_int64,
                                               C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.oracle_sinf_replica.restype = C.c_float
+        lib.oracle_sinf_replica.argtypes = [C.c_float]
+        lib.oracle_cosf_replica.restype = C.c_float
+        lib.oracle_cosf_replica.argtypes = [C.c_float]
+        lib.oracle_trig_mismatches.restype = C.c_int64
+        lib.oracle_trig_mismatches.argtypes = [C.c_float, C.c_float, C.c_uint32]
         lib.oracle_logp.restype = None
         lib.oracle_compute_returns.restype = None
         lib.oracle_logp.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int64, C.c_int64, C.c_int64,
@@ -529,3 +535,15 @@ def collect(world, cfg, params_tagger, params_runner, dims: PolicyDims, horizon:
     res = {k: np.stack(v) for k, v in out.items()}
     res["bootstrap"] = tag_policy_forward(world, cfg, params_tagger, params_runner, dims)[1].reshape(E, A)
     return res
+
+
+_LIBM_REPLICA = None
+
+
+def libm_matches_replica(stride: int = 997) -> bool:
+    """True when this host's libm sinf/cosf are the glibc FMA variant that the
+    device replica follows (checked on every `stride`-th float in [-2pi, 2pi])."""
+    global _LIBM_REPLICA
+    if _LIBM_REPLICA is None:
+        _LIBM_REPLICA = oracle_lib().oracle_trig_mismatches(0.0, 6.2831855, stride) == 0
+    return _LIBM_REPLICA

@@ -690,3 +690,74 @@ void oracle_compute_returns(const float* rewards, const uint8_t* done, const dou
     }
   }
 }
+
+/* ---- glibc sinf / cosf replica ------------------------------------------- */
+/* Coefficients of glibc's __sincosf_table (optimized-routines sincosf.h):
+ * table 1 is table 0 with the cos coefficients negated. */
+typedef struct {
+  double hpi_inv, hpi, c0, c1, s1, c2, s2, c3, s3, c4;
+} sincos_tab;
+static const sincos_tab k_sincos[2] = {
+    {0x1.45f306dc9c883p+23, 0x1.921fb54442d18p+0, 0x1.0p+0, -0x1.ffffffd0c621cp-2, -0x1.555545995a603p-3,
+     0x1.55553e1068f19p-5, 0x1.1107605230bc4p-7, -0x1.6c087e89a359dp-10, -0x1.994eb3774cf24p-13,
+     0x1.99343027bf8c3p-16},
+    {0x1.45f306dc9c883p+23, 0x1.921fb54442d18p+0, -0x1.0p+0, 0x1.ffffffd0c621cp-2, -0x1.555545995a603p-3,
+     -0x1.55553e1068f19p-5, 0x1.1107605230bc4p-7, 0x1.6c087e89a359dp-10, -0x1.994eb3774cf24p-13,
+     -0x1.99343027bf8c3p-16}};
+
+static double rep_sin_poly(double xs, double x2, const sincos_tab* p) {
+  const double a = fma(x2, p->s3, p->s2);
+  const double x3 = x2 * xs;
+  const double x5 = x2 * x3;
+  return fma(a, x5, fma(x3, p->s1, xs));
+}
+
+static double rep_cos_poly(double x2, const sincos_tab* p) {
+  const double x4 = x2 * x2;
+  const double a = fma(x2, p->c1, p->c0);
+  const double b = fma(x2, p->c4, p->c3);
+  const double x6 = x2 * x4;
+  return fma(b, x6, fma(x4, p->c2, a));
+}
+
+static float rep_sincosf(float y, int want_cos) {
+  uint32_t u;
+  memcpy(&u, &y, 4);
+  const uint32_t top = (u >> 20) & 0x7ffu;
+  const double x = (double)y;
+  if (top <= 0x3f3u) {
+    if (top <= 0x397u) return want_cos ? 1.0f : y;
+    const double x2 = x * x;
+    return (float)(want_cos ? rep_cos_poly(x2, &k_sincos[0]) : rep_sin_poly(x, x2, &k_sincos[0]));
+  }
+  if (top > 0x42eu) return want_cos ? cosf(y) : sinf(y);
+  const int n = (((int32_t)(x * k_sincos[0].hpi_inv)) + 0x800000) >> 24;
+  const double r = fma(-(double)n, k_sincos[0].hpi, x);
+  const sincos_tab* p = &k_sincos[(n & 2) ? 1 : 0];
+  const double x2 = r * r;
+  if ((((n & 1) == 0) ? 1 : 0) == want_cos) return (float)rep_cos_poly(x2, p);
+  const double sign = ((n + 1) & 2) ? -1.0 : 1.0;
+  return (float)rep_sin_poly(r * sign, x2, p);
+}
+
+float oracle_sinf_replica(float y) { return rep_sincosf(y, 0); }
+float oracle_cosf_replica(float y) { return rep_sincosf(y, 1); }
+
+int64_t oracle_trig_mismatches(float lo, float hi, uint32_t stride) {
+  uint32_t a, b;
+  memcpy(&a, &lo, 4);
+  memcpy(&b, &hi, 4);
+  int64_t bad = 0;
+  for (uint64_t w = a; w <= b; w += stride) {
+    float y;
+    const uint32_t u = (uint32_t)w;
+    memcpy(&y, &u, 4);
+    for (int sg = 0; sg < 2; ++sg) {
+      const float z = sg ? -y : y;
+      const float s = sinf(z), c = cosf(z);
+      if (memcmp(&s, &(float){oracle_sinf_replica(z)}, 4) != 0) ++bad;
+      if (memcmp(&c, &(float){oracle_cosf_replica(z)}, 4) != 0) ++bad;
+    }
+  }
+  return bad;
+}

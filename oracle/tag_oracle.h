@@ -87,6 +87,15 @@ void oracle_logp(const double* logits, const int32_t* actions, int64_t rows, int
 void oracle_compute_returns(const float* rewards, const uint8_t* done, const double* bootstrap, int64_t T,
                             int64_t E, int64_t A, double gamma, double* returns);
 
+/* ---- glibc sinf / cosf replica ------------------- */
+/* The x86-64 glibc 2.39 FMA variant of sinf / cosf for |y| < 120 (the device
+ * replica in tag_kernels.cu follows the same steps); larger |y| calls libm. */
+float oracle_sinf_replica(float y);
+float oracle_cosf_replica(float y);
+/* Mismatches of the replica against this host's libm sinf / cosf over every
+ * `stride`-th float bit pattern in [lo, hi] and its negation. */
+int64_t oracle_trig_mismatches(float lo, float hi, uint32_t stride);
+
 #ifdef __cplusplus
 }
 #endif
