@@ -344,6 +344,34 @@ WDG_API wdg_status wdg_rollout_collect(wdg_rollout* rollout, wdg_batch* batch);
 WDG_API wdg_status wdg_compute_returns(const wdg_batch* batch, double gamma, double* device_returns,
                                        void* cuda_stream);
 
+/* ---- Session (proj/include/warp/warp_c.h:51-86) ------------------------- */
+/* The reference's session C ABI on the device path: a strict JSON RunConfig
+ * (harness.cpp:32-158,279-324; same keys, defaults, canonical JSON and FNV-1a
+ * config hash), run modes check / bench-envs / bench-agents driving the B200
+ * kernels, JSON report + summary, CSV reports under run.output_dir. Training
+ * (the reference's CPU learner) is out of scope: it returns WDG_ERR_STATE. */
+typedef struct wdg_session wdg_session;
+WDG_API wdg_status wdg_session_open(const char* config_json, wdg_session** out);      /* warp_c.h:55 */
+WDG_API wdg_status wdg_session_open_file(const char* path, wdg_session** out);        /* warp_c.h:56 */
+WDG_API void wdg_session_close(wdg_session* session);                                 /* warp_c.h:57 */
+WDG_API wdg_status wdg_session_set_seed(wdg_session* session, uint64_t seed);         /* warp_c.h:61 */
+WDG_API wdg_status wdg_session_set_workers(wdg_session* session, int32_t workers);    /* warp_c.h:62 */
+WDG_API wdg_status wdg_session_set_output_dir(wdg_session* session, const char* dir); /* warp_c.h:63 */
+WDG_API const char* wdg_session_config_json(wdg_session* session);                    /* warp_c.h:66 */
+WDG_API const char* wdg_session_config_hash(wdg_session* session);                    /* warp_c.h:67 */
+/* check (harness.cpp:563-660): per variant x obs mode, the fused one-kernel
+ * rollout and the unfused kernel sequence in lockstep with the same f64
+ * policy, stores compared on device each step in the reference's causal
+ * order; WDG_ERR_STATE on a divergence (c_api.cpp:177-191). */
+WDG_API wdg_status wdg_session_run_check(wdg_session* session);                       /* warp_c.h:73 */
+WDG_API wdg_status wdg_session_run_bench_envs(wdg_session* session);                  /* warp_c.h:74 */
+WDG_API wdg_status wdg_session_run_bench_agents(wdg_session* session);                /* warp_c.h:75 */
+WDG_API wdg_status wdg_session_run_training(wdg_session* session);                    /* warp_c.h:76 */
+WDG_API const char* wdg_session_report_json(wdg_session* session);                    /* warp_c.h:79 */
+WDG_API const char* wdg_session_summary(wdg_session* session);                        /* warp_c.h:80 */
+WDG_API wdg_status wdg_session_dump_array(wdg_session* session, const char* array_name,
+                                          const char* csv_path);                      /* warp_c.h:85-86 */
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

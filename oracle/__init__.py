@@ -201,6 +201,9 @@ def ref_lib():
         lib.ref_bench_sharded.restype = C.c_int
         lib.ref_bench_sharded.argtypes = [C.POINTER(TagConfigC), C.c_int64, C.c_int, C.c_int64, C.c_int64,
                                           C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        if hasattr(lib, "ref_config_canonical"):
+            lib.ref_config_canonical.restype = C.c_int64
+            lib.ref_config_canonical.argtypes = [C.c_char_p, C.c_int32, C.c_char_p, C.c_int64]
         I64P = C.POINTER(C.c_int64)
         lib.ref_policy_init.restype = C.c_int
         lib.ref_policy_init.argtypes = [C.c_uint64, C.c_int64, I64P, C.c_int32, C.c_int64, C.c_int64,
@@ -547,3 +550,14 @@ def libm_matches_replica(stride: int = 997) -> bool:
     if _LIBM_REPLICA is None:
         _LIBM_REPLICA = oracle_lib().oracle_trig_mismatches(0.0, 6.2831855, stride) == 0
     return _LIBM_REPLICA
+
+
+def ref_config_canonical(text: str, hash: bool = False):
+    """The reference's RunConfig::from_string(text).to_json_string() /
+    config_hash() (harness.cpp:279-322); (status, string)."""
+    lib = ref_lib()
+    if not hasattr(lib, "ref_config_canonical"):
+        return None, None
+    buf = C.create_string_buffer(1 << 16)
+    n = lib.ref_config_canonical(text.encode(), 1 if hash else 0, buf, len(buf))
+    return (0, buf.value.decode()) if n >= 0 else (int(-n), None)

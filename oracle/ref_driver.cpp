@@ -17,6 +17,9 @@
 #include <thread>
 #include <vector>
 
+#ifdef REF_HAVE_HARNESS
+#include "warp/harness.hpp"
+#endif
 #include "warp/policy_model.hpp"
 #include "warp/trainer.hpp"
 #include "warp/data_store.hpp"
@@ -363,5 +366,25 @@ __attribute__((visibility("default"))) int ref_compute_returns(const float* rewa
     return 0;
   });
 }
+
+#ifdef REF_HAVE_HARNESS
+// RunConfig::from_string -> to_json_string() / config_hash() (harness.cpp:
+// 279-322): the canonical form the session ABI must reproduce. Writes a
+// NUL-terminated string; returns its length or a negative status.
+__attribute__((visibility("default"))) int64_t ref_config_canonical(const char* text, int32_t hash,
+                                                                    char* out, int64_t cap) {
+  try {
+    const warp::RunConfig c = warp::RunConfig::from_string(text);
+    c.validate();
+    const std::string s = hash ? c.config_hash() : c.to_json_string();
+    if (static_cast<int64_t>(s.size()) + 1 > cap) return -1000;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return static_cast<int64_t>(s.size());
+  } catch (const warp::Error& e) {
+    g_err = e.what();
+    return -static_cast<int64_t>(e.code());
+  }
+}
+#endif
 
 }  // extern "C"

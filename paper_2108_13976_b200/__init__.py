@@ -74,6 +74,11 @@ EXPORTED_SYMBOLS = [
     "wdg_policy_set_params", "wdg_policy_get_params", "wdg_policy_forward", "wdg_rollout_set_policies",
     "wdg_rollout_policy_outputs", "wdg_copy_to_host", "wdg_rollout_set_keep_policy_outputs",
     "wdg_batch_create", "wdg_batch_destroy", "wdg_batch_get_view", "wdg_rollout_collect", "wdg_compute_returns",
+    "wdg_session_open", "wdg_session_open_file", "wdg_session_close", "wdg_session_set_seed",
+    "wdg_session_set_workers", "wdg_session_set_output_dir", "wdg_session_config_json",
+    "wdg_session_config_hash", "wdg_session_run_check", "wdg_session_run_bench_envs",
+    "wdg_session_run_bench_agents", "wdg_session_run_training", "wdg_session_report_json",
+    "wdg_session_summary", "wdg_session_dump_array",
 ]
 
 POLICY_F64, POLICY_BF16 = 0, 1
@@ -200,6 +205,21 @@ def _load():
         "wdg_batch_get_view": (I32, [P, C.POINTER(_BatchViewC)]),
         "wdg_rollout_collect": (I32, [P, P]),
         "wdg_compute_returns": (I32, [P, D, P, P]),
+        "wdg_session_open": (I32, [C.c_char_p, C.POINTER(P)]),
+        "wdg_session_open_file": (I32, [C.c_char_p, C.POINTER(P)]),
+        "wdg_session_close": (None, [P]),
+        "wdg_session_set_seed": (I32, [P, U64]),
+        "wdg_session_set_workers": (I32, [P, I32]),
+        "wdg_session_set_output_dir": (I32, [P, C.c_char_p]),
+        "wdg_session_config_json": (C.c_char_p, [P]),
+        "wdg_session_config_hash": (C.c_char_p, [P]),
+        "wdg_session_run_check": (I32, [P]),
+        "wdg_session_run_bench_envs": (I32, [P]),
+        "wdg_session_run_bench_agents": (I32, [P]),
+        "wdg_session_run_training": (I32, [P]),
+        "wdg_session_report_json": (C.c_char_p, [P]),
+        "wdg_session_summary": (C.c_char_p, [P]),
+        "wdg_session_dump_array": (I32, [P, C.c_char_p, C.c_char_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -766,6 +786,65 @@ class RolloutBatch:
         st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
         _check(self._lib.wdg_compute_returns(self._h, float(gamma), C.c_void_p(_ptr(out)), st))
         return out
+
+
+class Session:
+    """wd_session (proj/include/warp/warp_c.h:51-86) on the device path."""
+
+    def __init__(self, config_json: str = "{}", path: Optional[str] = None):
+        self._lib = _load()
+        h = C.c_void_p()
+        if path is not None:
+            _check(self._lib.wdg_session_open_file(path.encode(), C.byref(h)))
+        else:
+            _check(self._lib.wdg_session_open(config_json.encode(), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wdg_session_close(self._h)
+            self._h = None
+
+    def set_seed(self, seed: int):
+        _check(self._lib.wdg_session_set_seed(self._h, int(seed)))
+
+    def set_workers(self, workers: int):
+        _check(self._lib.wdg_session_set_workers(self._h, int(workers)))
+
+    def set_output_dir(self, d: str):
+        _check(self._lib.wdg_session_set_output_dir(self._h, d.encode()))
+
+    def config_json(self) -> str:
+        return self._lib.wdg_session_config_json(self._h).decode()
+
+    def config_hash(self) -> str:
+        return self._lib.wdg_session_config_hash(self._h).decode()
+
+    def run_check(self):
+        _check(self._lib.wdg_session_run_check(self._h))
+
+    def run_bench_envs(self):
+        _check(self._lib.wdg_session_run_bench_envs(self._h))
+
+    def run_bench_agents(self):
+        _check(self._lib.wdg_session_run_bench_agents(self._h))
+
+    def run_training(self):
+        _check(self._lib.wdg_session_run_training(self._h))
+
+    def report_json(self) -> Optional[str]:
+        r = self._lib.wdg_session_report_json(self._h)
+        return r.decode() if r else None
+
+    def summary(self) -> Optional[str]:
+        r = self._lib.wdg_session_summary(self._h)
+        return r.decode() if r else None
+
+    def dump_array(self, name: str, csv_path: str):
+        _check(self._lib.wdg_session_dump_array(self._h, name.encode(), csv_path.encode()))
 
 
 class Workspace:

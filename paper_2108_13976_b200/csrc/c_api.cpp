@@ -3,6 +3,8 @@
 // guarded, exceptions map 1:1 onto status codes, the message is kept in a
 // thread-local buffer returned by wdg_last_error().
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <memory>
 #include <string>
 
@@ -27,6 +29,10 @@ struct wdg_policy {
 };
 struct wdg_batch {
   std::unique_ptr<wdg::RolloutBatch> impl;
+};
+struct wdg_session {
+  wdg::Session* impl = nullptr;
+  ~wdg_session() { wdg::session_close(impl); }
 };
 
 namespace {
@@ -538,6 +544,119 @@ wdg_status wdg_compute_returns(const wdg_batch* batch, double gamma, double* dev
                          static_cast<cudaStream_t>(cuda_stream));
     wdg::cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(cuda_stream)), "compute_returns");
   });
+}
+
+// ---- session (c_api.cpp:97-255 of the reference) ----------------------------
+wdg_status wdg_session_open(const char* config_json, wdg_session** out) {
+  if (config_json == nullptr || out == nullptr) {
+    g_last_error = "null argument";
+    return WDG_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] {
+    auto s = std::make_unique<wdg_session>();
+    s->impl = wdg::session_open(config_json);
+    *out = s.release();
+  });
+}
+
+wdg_status wdg_session_open_file(const char* path, wdg_session** out) {
+  if (path == nullptr || out == nullptr) {
+    g_last_error = "null argument";
+    return WDG_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] {
+    std::ifstream is(path);
+    if (!is) wdg::raise(wdg::Errc::io_error, std::string("cannot open config file: ") + path);
+    std::stringstream ss;
+    ss << is.rdbuf();
+    auto s = std::make_unique<wdg_session>();
+    s->impl = wdg::session_open(ss.str());
+    *out = s.release();
+  });
+}
+
+void wdg_session_close(wdg_session* session) { delete session; }
+
+namespace {
+wdg::Session* sess(wdg_session* s) {
+  if (s == nullptr || s->impl == nullptr) wdg::raise(wdg::Errc::invalid_argument, "null session");
+  return s->impl;
+}
+}  // namespace
+
+wdg_status wdg_session_set_seed(wdg_session* session, uint64_t seed) {
+  return guarded([&] { wdg::session_set_seed(sess(session), seed); });
+}
+
+wdg_status wdg_session_set_workers(wdg_session* session, int32_t workers) {
+  return guarded([&] { wdg::session_set_workers(sess(session), workers); });
+}
+
+wdg_status wdg_session_set_output_dir(wdg_session* session, const char* dir) {
+  return guarded([&] {
+    if (dir == nullptr) wdg::raise(wdg::Errc::invalid_argument, "null output dir");
+    wdg::session_set_output_dir(sess(session), dir);
+  });
+}
+
+const char* wdg_session_config_json(wdg_session* session) {
+  const char* r = nullptr;
+  guarded([&] { r = wdg::session_config_json(sess(session)); });
+  return r;
+}
+
+const char* wdg_session_config_hash(wdg_session* session) {
+  const char* r = nullptr;
+  guarded([&] { r = wdg::session_config_hash(sess(session)); });
+  return r;
+}
+
+wdg_status wdg_session_run_check(wdg_session* session) {
+  bool passed = true;
+  const wdg_status st = guarded([&] { passed = wdg::session_run_check(sess(session)); });
+  if (st != WDG_OK) return st;
+  if (!passed) {
+    g_last_error = "consistency check failed; see report for first divergence";
+    return WDG_ERR_STATE;
+  }
+  return WDG_OK;
+}
+
+wdg_status wdg_session_run_bench_envs(wdg_session* session) {
+  return guarded([&] { wdg::session_run_bench_envs(sess(session)); });
+}
+
+wdg_status wdg_session_run_bench_agents(wdg_session* session) {
+  return guarded([&] { wdg::session_run_bench_agents(sess(session)); });
+}
+
+wdg_status wdg_session_run_training(wdg_session* session) {
+  return guarded([&] {
+    sess(session);
+    wdg::raise(wdg::Errc::state_error,
+               "training (the reference's CPU learner) is out of scope on the device path; "
+               "use wdg_rollout_collect + wdg_compute_returns for device rollouts");
+  });
+}
+
+const char* wdg_session_report_json(wdg_session* session) {
+  const char* r = nullptr;
+  guarded([&] { r = wdg::session_report_json(sess(session)); });
+  return r;
+}
+
+const char* wdg_session_summary(wdg_session* session) {
+  const char* r = nullptr;
+  guarded([&] { r = wdg::session_summary(sess(session)); });
+  return r;
+}
+
+wdg_status wdg_session_dump_array(wdg_session* session, const char* array_name, const char* csv_path) {
+  if (array_name == nullptr || csv_path == nullptr) {
+    g_last_error = "null argument";
+    return WDG_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] { wdg::session_dump_array(sess(session), array_name, csv_path); });
 }
 
 }  // extern "C"

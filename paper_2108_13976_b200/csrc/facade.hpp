@@ -273,6 +273,23 @@ class Rollout {
   cudaStream_t graph_stream_ = nullptr;  // mix64(substream(seed, kStreamActions))
 };
 
+// Session layer (session.cpp): the reference's wd_session_* run modes on the
+// device path (c_api.cpp:97-255, harness.cpp:32-335,563-898).
+struct Session;
+Session* session_open(const std::string& config_json);
+const char* session_config_json(Session* s);
+const char* session_config_hash(Session* s);
+void session_set_seed(Session* s, uint64_t seed);
+void session_set_workers(Session* s, int32_t workers);
+void session_set_output_dir(Session* s, const std::string& dir);
+bool session_run_check(Session* s);
+void session_run_bench_envs(Session* s);
+void session_run_bench_agents(Session* s);
+const char* session_report_json(Session* s);
+const char* session_summary(Session* s);
+void session_dump_array(Session* s, const std::string& name, const std::string& path);
+void session_close(Session* s);
+
 // Host-side RNG prefix helpers (rng.hpp:23-53).
 uint64_t host_mix64(uint64_t x);
 uint64_t host_absorb(uint64_t h, uint64_t v);

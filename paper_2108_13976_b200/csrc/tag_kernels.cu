@@ -786,8 +786,9 @@ __device__ __forceinline__ void write_row(const EnvSmem& s, const TagDevConfig& 
 // via (int)(x * 2^24 * 2/pi) + 2^23 >> 24, r = fma(-n, pi/2, x), then the
 // sin or cos polynomial of r with coefficient table n & 2 and sign n & 3 — every
 // a*b+c fused exactly where the FMA build fuses it (read off the shipped
-// libm.so.6, s_sinf-fma / s_cosf-fma). tests/test_trig.py checks this replica
-// (oracle/tag_oracle.c) against the host libm on every float in [-2pi, 2pi].
+// libm.so.6, s_sinf-fma / s_cosf-fma). tests/test_trig.py checks the same
+// steps, restated in C for the tests, against the host libm on every float in
+// [-2pi, 2pi].
 // |x| >= 120 (never produced by the env: directions stay in [0, 2pi)) uses
 // the f64 sin/cos rounded once.
 struct SinCosTab {
