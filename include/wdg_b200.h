@@ -253,6 +253,8 @@ WDG_API wdg_status wdg_rollout_step_host(wdg_rollout* rollout, const double* hos
                                          uint8_t* host_done);
 WDG_API wdg_status wdg_rollout_run(wdg_rollout* rollout, int64_t steps);
 WDG_API wdg_status wdg_rollout_next_step(const wdg_rollout* rollout, int64_t* out);
+/* Kernel launches issued so far (step kernels, policy forwards, graph nodes). */
+WDG_API wdg_status wdg_rollout_launches(const wdg_rollout* rollout, int64_t* out);
 /* Synchronise and surface sticky device errors (non-finite logits seen by the
  * fused sampler) as WDG_ERR_NON_FINITE. */
 WDG_API wdg_status wdg_rollout_check(wdg_rollout* rollout);

@@ -78,7 +78,7 @@ EXPORTED_SYMBOLS = [
     "wdg_session_set_workers", "wdg_session_set_output_dir", "wdg_session_config_json",
     "wdg_session_config_hash", "wdg_session_run_check", "wdg_session_run_bench_envs",
     "wdg_session_run_bench_agents", "wdg_session_run_training", "wdg_session_report_json",
-    "wdg_session_summary", "wdg_session_dump_array",
+    "wdg_session_summary", "wdg_session_dump_array", "wdg_rollout_launches",
 ]
 
 POLICY_F64, POLICY_BF16 = 0, 1
@@ -220,6 +220,7 @@ def _load():
         "wdg_session_report_json": (C.c_char_p, [P]),
         "wdg_session_summary": (C.c_char_p, [P]),
         "wdg_session_dump_array": (I32, [P, C.c_char_p, C.c_char_p]),
+        "wdg_rollout_launches": (I32, [P, C.POINTER(I64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -664,6 +665,11 @@ class RolloutDriver:
 
     def run(self, steps: int):
         _check(self._lib.wdg_rollout_run(self._h, steps))
+
+    def launches(self) -> int:
+        v = C.c_int64()
+        _check(self._lib.wdg_rollout_launches(self._h, C.byref(v)))
+        return v.value
 
     def next_step(self) -> int:
         v = C.c_int64()

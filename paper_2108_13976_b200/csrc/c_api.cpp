@@ -659,4 +659,8 @@ wdg_status wdg_session_dump_array(wdg_session* session, const char* array_name, 
   return guarded([&] { wdg::session_dump_array(sess(session), array_name, csv_path); });
 }
 
+wdg_status wdg_rollout_launches(const wdg_rollout* r, int64_t* out) {
+  return guarded([&] { *need(out, "out") = need(r, "rollout")->impl->launches(); });
+}
+
 }  // extern "C"

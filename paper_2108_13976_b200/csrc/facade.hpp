@@ -150,6 +150,8 @@ class TagPlan {
   void run_step(int64_t step_index);
   void reinit_masked(const uint8_t* env_mask, int32_t* episode);
   void launch(TagLaunch L);
+  // Whether RolloutDriver::run may use multi-step residency launches.
+  bool multistep_ok();
   const wdg_tag_config& config() const { return cfg_; }
   const TagDevConfig& dev() const { return dev_; }
   DataStore& store() { return store_; }
@@ -159,6 +161,7 @@ class TagPlan {
   wdg_tag_config cfg_;
   TagDevConfig dev_;
   TagDevArrays arrays_;
+  int multistep_ = -1;
 };
 
 // sample_actions (sampler.hpp:35-36) with device logits.
@@ -225,6 +228,9 @@ class Rollout {
   void run(int64_t steps);
   void reduce_stats_into(double* device_out);
   int64_t next_step() const { return t_; }
+  // Kernel launches this driver has issued (env step kernels, policy
+  // forwards, graph replays counted per node).
+  int64_t launches() const { return launches_; }
   void check();
   void stats(double* out, int32_t count);
   void reset_stats();
@@ -248,6 +254,7 @@ class Rollout {
   ResetManager* resets_;
   uint64_t seed_;
   int64_t t_ = 0;
+  int64_t launches_ = 0;
   bool fused_ = true;
   bool graphs_ = true;
   const double* logits_ = nullptr;
@@ -266,6 +273,7 @@ class Rollout {
   void build_graph();
   void drop_graph();
   static constexpr int kGraphSteps = 16;
+  static constexpr int kMultiSteps = 64;  // steps per multi-step residency launch
   cudaGraphExec_t graph_exec_ = nullptr;
   int64_t* step_dev_ = nullptr;
   const double* graph_logits_ = nullptr;

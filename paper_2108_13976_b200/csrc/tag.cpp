@@ -341,6 +341,28 @@ void TagPlan::launch(TagLaunch L) {
   cuda_check(launch_tag_kernel(dev_, arrays_, L, store_.stream()), "tag kernel launch");
 }
 
+// Multi-step residency pays everywhere measured except the generic ring
+// K-NN (continuous / non-lattice discrete partial obs) at fewer than 3 waves
+// of CTAs, where it measured 2-18% slower (profiles/sweep_multistep_r01.json).
+bool TagPlan::multistep_ok() {
+  if (multistep_ < 0) {
+    multistep_ = 1;
+    if (dev_.use_grid && dev_.partial && !dev_.lattice) {
+      uint32_t per_sm = 0;
+      TagLaunch q;
+      q.mode = -1;  // occupancy query
+      q.error = &per_sm;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const bool ok = launch_tag_kernel(dev_, arrays_, q, store_.stream()) == cudaSuccess && per_sm > 0;
+      const double waves = ok ? static_cast<double>(dev_.grid_ctas) / (static_cast<double>(sms) * per_sm) : 0.0;
+      multistep_ = waves >= 3.0 ? 1 : 0;
+    }
+  }
+  return multistep_ == 1;
+}
+
 void TagPlan::run_step(int64_t step_index) {
   (void)step_index;  // the Tag kernels do not use the step index (tag_env.cpp:530)
   TagLaunch L;
@@ -634,6 +656,7 @@ void Rollout::set_policies(const Policy* tagger, const Policy* runner, int32_t p
 void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add,
                                double* values_out, bool force_logits, bool sample) {
   if (pol_[0] == nullptr) return;
+  if (step_dev == nullptr) launches_ += pol_[0] == pol_[1] ? 1 : 2;
   const TagDevConfig& p = plan_.dev();
   const float* obs = static_cast<const float*>(store_.device_ptr(store_.handle(kObservations)));
   // f64 logits are the sampler's input (always written); bf16 samples in the
@@ -707,12 +730,14 @@ void Rollout::step_unfused() {
              "sample kernel");
   plan_.run_step(t_);
   if (resets_ != nullptr && resets_->auto_enabled()) resets_->auto_reset_on_done();
+  launches_ += policy_samples() ? 1 : 2;  // (+ the reset kernels, counted in the ResetManager's own launches)
 }
 
 void Rollout::step() {
   forward_policies(store_.stream(), t_, nullptr, 0, nullptr, false, true);
   if (fused_ok()) {
     plan_.launch(fused_launch(t_));
+    ++launches_;
   } else {
     step_unfused();
   }
@@ -824,6 +849,25 @@ void Rollout::build_graph() {
 
 void Rollout::run(int64_t steps) {
   if (steps < 0) raise(Errc::invalid_argument, "rollout run: steps must be >= 0");
+  // Multi-step residency: with a fixed logits buffer (no policy between
+  // steps) consecutive steps are independent launches of the same kernel on
+  // the same env, so one launch runs up to kMultiSteps of them with each
+  // env's state kept in shared memory (TagLaunch::n_steps).
+  static const bool multi_off = std::getenv("WDG_NO_MULTISTEP") != nullptr;
+  if (!multi_off && fused_ok() && pol_[0] == nullptr && steps > 1 && plan_.multistep_ok()) {
+    while (steps > 0) {
+      const int32_t k = static_cast<int32_t>(std::min<int64_t>(steps, kMultiSteps));
+      TagLaunch L = fused_launch(t_);
+      L.n_steps = k;
+      L.step0 = t_;
+      L.action_h0 = h_actions0_;
+      plan_.launch(L);
+      ++launches_;
+      t_ += k;
+      steps -= k;
+    }
+    return;
+  }
   if (graphs_ && fused_ok() && steps >= kGraphSteps) {
     if (graph_exec_ == nullptr || graph_logits_ != logits_ || graph_pol_version_ != pol_version_ ||
         graph_bias_ != fault_tag_radius_bias() ||
@@ -833,6 +877,7 @@ void Rollout::run(int64_t steps) {
     while (steps >= kGraphSteps) {
       cuda_check(launch_set_counter(step_dev_, t_, store_.stream()), "set step counter");
       cuda_check(cudaGraphLaunch(graph_exec_, store_.stream()), "graph launch");
+      launches_ += 1 + kGraphSteps * (pol_[0] != nullptr ? (pol_[0] == pol_[1] ? 2 : 3) : 1);
       t_ += kGraphSteps;
       steps -= kGraphSteps;
     }

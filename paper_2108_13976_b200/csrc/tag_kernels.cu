@@ -1117,6 +1117,12 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   // flags) vector and the logits rows of a thread are contiguous.
   const bool vec4 = GRID && (A & 3) == 0;
 
+  const int n_steps = (mode == kModeFused && sample_here) ? L.n_steps : 1;
+  for (int it = 0; it < n_steps; ++it) {
+  // Iteration `it` of a multi-step launch: step L.step0 + it. After the first,
+  // the env's state is already in shared memory (written by the previous
+  // iteration); only the step's logits are read.
+  const bool first = it == 0;
   // Phase 0: stage the env's agent state in shared memory.
   bool integral = true;
   bool nonfinite = false;
@@ -1130,7 +1136,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     // (tag_env.cpp:148-160) run from registers and the moved state lands in
     // shared memory once.
     const uint64_t h_step =
-        L.step_dev != nullptr
+        n_steps > 1 ? absorb(L.action_h0, static_cast<uint64_t>(L.step0 + it))
+        : L.step_dev != nullptr
             ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
             : L.action_h_step;
     const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
@@ -1145,14 +1152,16 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       if (tid == 0) {
         const uint32_t rowb = static_cast<uint32_t>(A) * 4u;
         const uint32_t lgb = sample_here ? static_cast<uint32_t>(A) * kC * kV * 8u : 0u;
-        mbar_init(bar, 1);
-        mbar_expect_tx(bar, lgb + (CONT ? 4u : 2u) * rowb);
+        if (first) mbar_init(bar, 1);
+        mbar_expect_tx(bar, lgb + (first ? (CONT ? 4u : 2u) * rowb : 0u));
         if (lgb) bulk_g2s(smem + p.off_zone, L.logits + ga * kC * kV, lgb, bar);
-        bulk_g2s(s.x, g.loc_x + ga, rowb, bar);
-        bulk_g2s(s.y, g.loc_y + ga, rowb, bar);
-        if (CONT) {
-          bulk_g2s(s.sp, g.speed + ga, rowb, bar);
-          bulk_g2s(s.dir, g.direction + ga, rowb, bar);
+        if (first) {
+          bulk_g2s(s.x, g.loc_x + ga, rowb, bar);
+          bulk_g2s(s.y, g.loc_y + ga, rowb, bar);
+          if (CONT) {
+            bulk_g2s(s.sp, g.speed + ga, rowb, bar);
+            bulk_g2s(s.dir, g.direction + ga, rowb, bar);
+          }
         }
         // L2 prefetch of the inputs of the env that will start about one CTA
         // lifetime from now (the next wave: `prefetch_stride` resident CTAs
@@ -1165,22 +1174,25 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           bulk_prefetch_l2(g.loc_y + pa, rowb);
         }
       }
-      __syncthreads();  // barrier initialised before anyone waits on it
-      mbar_wait(bar, 0);
+      if (first) __syncthreads();  // barrier initialised before anyone waits on it
+      mbar_wait(bar, static_cast<uint32_t>(it & 1));
     }
     for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
-      const float4 x4 = bulk ? *reinterpret_cast<const float4*>(s.x + a0)
-                             : *reinterpret_cast<const float4*>(g.loc_x + ga + a0);
-      const float4 y4 = bulk ? *reinterpret_cast<const float4*>(s.y + a0)
-                             : *reinterpret_cast<const float4*>(g.loc_y + ga + a0);
-      const uint32_t act4 = *reinterpret_cast<const uint32_t*>(g.active + ga + a0);
-      const uint32_t tag4 = *reinterpret_cast<const uint32_t*>(g.is_tagger + ga + a0);
+      const bool in_smem = bulk || !first;  // state already staged in shared memory
+      const float4 x4 = in_smem ? *reinterpret_cast<const float4*>(s.x + a0)
+                                : *reinterpret_cast<const float4*>(g.loc_x + ga + a0);
+      const float4 y4 = in_smem ? *reinterpret_cast<const float4*>(s.y + a0)
+                                : *reinterpret_cast<const float4*>(g.loc_y + ga + a0);
+      const uint32_t act4 = first ? *reinterpret_cast<const uint32_t*>(g.active + ga + a0)
+                                  : *reinterpret_cast<const uint32_t*>(s.act + a0);
+      const uint32_t tag4 = first ? *reinterpret_cast<const uint32_t*>(g.is_tagger + ga + a0)
+                                  : *reinterpret_cast<const uint32_t*>(s.tag + a0);
       float4 sp4 = make_float4(0.f, 0.f, 0.f, 0.f), dir4 = sp4;
       if (CONT) {
-        sp4 = bulk ? *reinterpret_cast<const float4*>(s.sp + a0)
-                   : *reinterpret_cast<const float4*>(g.speed + ga + a0);
-        dir4 = bulk ? *reinterpret_cast<const float4*>(s.dir + a0)
-                    : *reinterpret_cast<const float4*>(g.direction + ga + a0);
+        sp4 = in_smem ? *reinterpret_cast<const float4*>(s.sp + a0)
+                      : *reinterpret_cast<const float4*>(g.speed + ga + a0);
+        dir4 = in_smem ? *reinterpret_cast<const float4*>(s.dir + a0)
+                       : *reinterpret_cast<const float4*>(g.direction + ga + a0);
       }
       int32_t act0[4], act1[4] = {1, 1, 1, 1};
       if (sample_here) {
@@ -1324,19 +1336,20 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     uint64_t h_env = 0;
     if (!vec4 && mode != kModeReinit && sample_here) {
       const uint64_t h_step =
-          L.step_dev != nullptr
+          n_steps > 1 ? absorb(L.action_h0, static_cast<uint64_t>(L.step0 + it))
+          : L.step_dev != nullptr
               ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
               : L.action_h_step;
       h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
     }
     for (int a = vec4 ? A : lt; a < A; a += tpe) {
       if (mode != kModeReinit) {
-        float x = g.loc_x[ga + a], y = g.loc_y[ga + a];
-        const uint8_t act = g.active[ga + a];
+        float x = first ? g.loc_x[ga + a] : s.x[a], y = first ? g.loc_y[ga + a] : s.y[a];
+        const uint8_t act = first ? g.active[ga + a] : s.act[a];
         float sp = 0.f, dir = 0.f;
         if (CONT) {
-          sp = g.speed[ga + a];
-          dir = g.direction[ga + a];
+          sp = first ? g.speed[ga + a] : s.sp[a];
+          dir = first ? g.direction[ga + a] : s.dir[a];
         }
         integral &= (x == truncf(x)) && (y == truncf(y)) && x >= 0.0f && y >= 0.0f &&
                     x <= p.world_hi && y <= p.world_hi;
@@ -1368,16 +1381,18 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           s.dir[a] = dir;
         }
       }
-      s.tag[a] = g.is_tagger[ga + a];
+      if (first) s.tag[a] = g.is_tagger[ga + a];
       s.cred[a] = 0;
       s.tagged[a] = 0;
     }
     if (!vec4 && nonfinite && L.error) atomicOr(L.error, kErrNonFinite);
     if (lt == 0) {
       sc.runners_left = 0;
-      sc.step_count = pre_step;
+      if (first) {
+        sc.step_count = pre_step;
+        sc.episode = pre_episode;
+      }
       sc.done = 0;
-      sc.episode = pre_episode;
       sc.tags = 0;
       sc.live = 1;
       sc.lattice_ok = 1;
@@ -1534,10 +1549,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         }
       }
       double* es = L.env_stats + e * 8;
-      const double run_t = (GRID ? es[0] : pre_es[0]) + st;
-      const double run_r = (GRID ? es[1] : pre_es[1]) + sr;
-      es[5] = (GRID ? es[5] : pre_es[2]) + sc.tags;
-      es[6] = (GRID ? es[6] : pre_es[3]) + 1.0;
+      const bool pre = !GRID && first;  // the prefetched slots are current only on the first step
+      const double run_t = (pre ? pre_es[0] : es[0]) + st;
+      const double run_r = (pre ? pre_es[1] : es[1]) + sr;
+      es[5] = (pre ? pre_es[2] : es[5]) + sc.tags;
+      es[6] = (pre ? pre_es[3] : es[6]) + 1.0;
       if (sc.done) {
         es[2] += 1.0;
         es[3] += run_t;
@@ -1828,6 +1844,8 @@ obs_done:
       if (place && L.episode != nullptr) L.episode[e] = episode;
     }
   }
+  if (n_steps > 1) __syncthreads();  // the next step rewrites the shared state
+  }  // multi-step loop
 }
 
 // ---- standalone sampler: sample_actions (sampler.cpp:5-40) ----------------
@@ -1965,6 +1983,16 @@ template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT>
 cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                            cudaStream_t st) {
   auto kern = tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT>;
+  if (L.mode < 0) {  // occupancy query (kModeQuery): resident CTAs per SM -> *L.error
+    if (p.smem_bytes > 48 * 1024) {
+      cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+      if (err != cudaSuccess) return err;
+    }
+    int n = 0;
+    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, p.threads, p.smem_bytes);
+    *L.error = static_cast<uint32_t>(n);
+    return err;
+  }
   if (!CONT && GRID) {
     cudaError_t err = ensure_shell_table();
     if (err != cudaSuccess) return err;

@@ -109,6 +109,12 @@ struct TagLaunch {
   int32_t step_add = 0;
   uint64_t action_h0 = 0;
   const double* logits = nullptr;
+  // Multi-step residency (RolloutDriver::run, harness.cpp:492-494): n_steps > 1
+  // runs steps step0 .. step0 + n_steps - 1 in ONE launch, each env's state
+  // staying in shared memory between steps (fused mode with a logits buffer
+  // only). Every step still reads its logits and writes every output.
+  int32_t n_steps = 1;
+  int64_t step0 = 0;
   const uint8_t* env_mask = nullptr;  // reinit: envs to reinit (nullptr = all)
   int32_t* episode = nullptr;         // per-env episode counter (device)
   // Per-env tracker slots [E][8]: run_tagger, run_runner, episodes,

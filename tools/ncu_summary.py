@@ -71,7 +71,10 @@ def main():
     cfg = "c2_fused"
     if "--config" in sys.argv:
         cfg = sys.argv[sys.argv.index("--config") + 1]
-    algo = 2000 * 164009
+    steps = 1
+    if "--steps-per-launch" in sys.argv:  # multi-step residency launches
+        steps = int(sys.argv[sys.argv.index("--steps-per-launch") + 1])
+    algo = 2000 * 164009 * steps
     if "--bytes-per-launch" in sys.argv:
         algo = float(sys.argv[sys.argv.index("--bytes-per-launch") + 1])
     ks = raw(rep)
@@ -98,6 +101,11 @@ def main():
         traffic = rd + wr  # bytes (unit-normalised in raw())
         lines += ["", f"DRAM traffic per launch: {traffic / 1e6:,.1f} MB vs algorithmic "
                       f"{algo / 1e6:,.1f} MB ({traffic / algo:.2f}x)"]
+        if steps > 1:
+            lines += [f"launch = {steps} env-steps (multi-step residency): per step "
+                      f"{traffic / steps / 1e6:,.1f} MB DRAM, {num(d.get('gpu__time_duration.sum')) / steps:,.2f} "
+                      "(duration unit) per step"]
+            traffic /= steps  # per env-step launch equivalent, as bench.py reports
     stalls = {k: num(v) for k, v in d.items()
               if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")}
     top = sorted(((v, k) for k, v in stalls.items() if v), reverse=True)[:10]
