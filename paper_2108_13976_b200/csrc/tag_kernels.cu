@@ -543,13 +543,23 @@ __device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<M
   const int gc = p.gc;
   const int cx = cell_coord<CONT>(sx, p), cy = cell_coord<CONT>(sy, p);
   const int maxr = max(max(cx, gc - 1 - cx), max(cy, gc - 1 - cy));
+  // Continuous: the agent's distance to its own cell's nearest edge tightens
+  // the ring bound, and whole cells whose rectangle is farther than the
+  // current K-th best are skipped. Both use cells widened by 1e-3 of a cell
+  // (float cell assignment) and a (1 - 1e-5) factor, so a skipped cell can
+  // never hold an admissible candidate, ties included.
+  const double cs = p.cell_size;
+  const double edge_in = CONT ? fmax(0.0, fmin(fmin(static_cast<double>(sx) - cx * cs, (cx + 1) * cs - sx),
+                                               fmin(static_cast<double>(sy) - cy * cs, (cy + 1) * cs - sy)) -
+                                                  1e-3 * cs)
+                              : 0.0;
   for (int r = 0; r <= maxr; ++r) {
     if (r > 0 && top.full()) {
       // Every point in rings >= r is farther than this bound (SURVEY.md §8a
       // a6; cf. the reference's ring margin, neighbor_grid.hpp:90-96).
       float lb2;
       if (CONT) {
-        const double lb = fmax(0.0, (r - 1) - 1e-3) * p.cell_size;
+        const double lb = fmax(0.0, (r - 1) - 1e-3) * cs + edge_in;
         lb2 = static_cast<float>(lb * lb * (1.0 - 1e-5));
       } else {
         const float lb = static_cast<float>((r - 1) * p.lattice_w + 1);
@@ -563,6 +573,13 @@ __device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<M
       const int step = edge ? 1 : max(x1 - x0, 1);
       for (int gx = x0; gx <= x1; gx += step) {
         if (gx < 0 || gx >= gc) continue;
+        if (CONT && r > 1 && top.full()) {
+          const double lo_x = (gx - 1e-3) * cs, hi_x = (gx + 1 + 1e-3) * cs;
+          const double lo_y = (gy - 1e-3) * cs, hi_y = (gy + 1 + 1e-3) * cs;
+          const double dx = fmax(0.0, fmax(lo_x - sx, sx - hi_x));
+          const double dy = fmax(0.0, fmax(lo_y - sy, sy - hi_y));
+          if (static_cast<float>((dx * dx + dy * dy) * (1.0 - 1e-5)) > top.wd) continue;
+        }
         const int c = gy * gc + gx;
         const int e = s.cstart[c + 1];
         for (int t = s.cstart[c]; t < e; ++t) {
@@ -629,7 +646,8 @@ __device__ __forceinline__ void knn_agent(const EnvSmem& s, const TagDevConfig& 
 // Tag resolution for one active runner: resolve kernel (tag_env.cpp:403-456)
 // / TagReference::step (tag_env.cpp:546-571). Returns the credited tagger or -1.
 template <bool CONT, bool GRID>
-__device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn, bool cell_tagger) {
+__device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn, bool cell_tagger,
+                           bool tag_prefix = false) {
   if (!CONT && GRID && cell_tagger) return s.cfill[s.cellof[rn]];
   const float rx = s.x[rn], ry = s.y[rn];
   const float bias = p.fault_bias;
@@ -672,7 +690,11 @@ __device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn, bool
     for (int gx = x0; gx <= x1; ++gx) {
       const int c = gy * p.gc + gx;
       const int e = s.cstart[c + 1];
-      for (int t = s.cstart[c]; t < e; ++t) consider(s.items[t]);
+      for (int t = s.cstart[c]; t < e; ++t) {
+        const int j = s.items[t];
+        if (tag_prefix && j >= p.T) break;  // index-sorted cell: only runners follow
+        consider(j);
+      }
     }
   }
   return best;
@@ -1286,8 +1308,14 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       float sps[4] = {sp4.x, sp4.y, sp4.z, sp4.w}, dirs[4] = {dir4.x, dir4.y, dir4.z, dir4.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        integral &= (xs[k] == truncf(xs[k])) && (ys[k] == truncf(ys[k])) && xs[k] >= 0.0f &&
-                    ys[k] >= 0.0f && xs[k] <= p.world_hi && ys[k] <= p.world_hi;
+        // CTA predicate: discrete -> positions integral (lattice K-NN valid);
+        // continuous -> taggers are exactly the index prefix [0, T) (the
+        // radius query may stop at the first non-tagger of an index-sorted cell)
+        if (CONT)
+          integral &= (((tag4 >> (8 * k)) & 0xffu) != 0) == (a0 + k < p.T);
+        else
+          integral &= (xs[k] == truncf(xs[k])) && (ys[k] == truncf(ys[k])) && xs[k] >= 0.0f &&
+                      ys[k] >= 0.0f && xs[k] <= p.world_hi && ys[k] <= p.world_hi;
         if ((act4 >> (8 * k)) & 0xffu)
           move_regs<CONT>(p, a0 + k, act0[k], act1[k], xs[k], ys[k], sps[k], dirs[k]);
       }
@@ -1351,8 +1379,9 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           sp = first ? g.speed[ga + a] : s.sp[a];
           dir = first ? g.direction[ga + a] : s.dir[a];
         }
-        integral &= (x == truncf(x)) && (y == truncf(y)) && x >= 0.0f && y >= 0.0f &&
-                    x <= p.world_hi && y <= p.world_hi;
+        if (!CONT)  // (continuous: the tagger-prefix predicate is taken below)
+          integral &= (x == truncf(x)) && (y == truncf(y)) && x >= 0.0f && y >= 0.0f &&
+                      x <= p.world_hi && y <= p.world_hi;
         const int64_t row = (ga + a) * kC;
         int32_t act0, act1 = 1;
         if (sample_here) {
@@ -1382,6 +1411,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         }
       }
       if (first) s.tag[a] = g.is_tagger[ga + a];
+      if (CONT) integral &= (s.tag[a] != 0) == (a < p.T);
       s.cred[a] = 0;
       s.tagged[a] = 0;
     }
@@ -1425,7 +1455,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       const int a = base + lt;
       const bool valid = live && a < A;
       const bool runner = valid && !s.tag[a] && s.act[a];
-      const int best = runner ? find_tagger<CONT, GRID>(s, p, a, cell_tagger) : -1;
+      const int best = runner ? find_tagger<CONT, GRID>(s, p, a, cell_tagger, CONT && all_integral) : -1;
       if (best >= 0) {
         s.act[a] = 0;
         s.tagged[a] = 1;
