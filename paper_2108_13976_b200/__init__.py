@@ -223,7 +223,12 @@ def _load():
         "wdg_rollout_launches": (I32, [P, C.POINTER(I64)]),
     }
     for name, (res, args) in sig.items():
-        fn = getattr(lib, name)
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            if os.environ.get("WDG_LIB_VARIANT"):  # older tuning builds lack newer entry points
+                continue
+            raise
         fn.restype = res
         fn.argtypes = args
     _lib = lib
