@@ -1200,12 +1200,6 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     // latency, then sample (sampler.hpp:18-30) and apply_move
     // (tag_env.cpp:148-160) run from registers and the moved state lands in
     // shared memory once.
-    const uint64_t h_step =
-        n_steps > 1 ? absorb(L.action_h0, static_cast<uint64_t>(L.step0 + it))
-        : L.step_dev != nullptr
-            ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
-            : L.action_h_step;
-    const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
     // Bulk path (one env per CTA): one thread arms an mbarrier and issues TMA
     // bulk copies of the env's contiguous rows — f64 logits (fused) into the
     // zone, positions (+ speed/direction) straight into their smem arrays —
@@ -1242,6 +1236,14 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       if (first) __syncthreads();  // barrier initialised before anyone waits on it
       mbar_wait(bar, static_cast<uint32_t>(it & 1));
     }
+    // The step's counter-RNG prefix, after the bulk copies are issued (under
+    // graph replay the step index is a device load).
+    const uint64_t h_step =
+        n_steps > 1 ? absorb(L.action_h0, static_cast<uint64_t>(L.step0 + it))
+        : L.step_dev != nullptr
+            ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
+            : L.action_h_step;
+    const uint64_t h_env = absorb(h_step, static_cast<uint64_t>(p.env_offset + e));
     for (int a0 = 4 * lt; a0 < A; a0 += 4 * tpe) {
       const bool in_smem = bulk || !first;  // state already staged in shared memory
       const float4 x4 = in_smem ? *reinterpret_cast<const float4*>(s.x + a0)
