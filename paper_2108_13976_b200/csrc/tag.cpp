@@ -350,10 +350,15 @@ void TagPlan::launch(TagLaunch L) {
 
 // Multi-step residency pays everywhere measured except the generic ring
 // K-NN (continuous / non-lattice discrete partial obs) at fewer than 3 waves
-// of CTAs, where it measured 2-18% slower (profiles/sweep_multistep_r01.json).
+// of CTAs, where it measured 2-18% slower, and grid-path full observations
+// (profiles/sweep_r01.json: single_step vs run_multistep).
 bool TagPlan::multistep_ok() {
   if (multistep_ < 0) {
     multistep_ = 1;
+    // full observations on the grid path: the looped (multi-step) build of
+    // the wide-row writer is 6-9% slower than the single-step build
+    // (profiles/sweep_r01.json), which outweighs the saved state reloads
+    if (dev_.use_grid && !dev_.partial) multistep_ = 0;
     if (dev_.use_grid && dev_.partial && !dev_.lattice) {
       uint32_t per_sm = 0;
       TagLaunch q;
