@@ -355,7 +355,10 @@ __device__ __forceinline__ int sample_row_regs(const double* z, double u) {
 // KP: layer-1 K (obs_dim padded to 16); C x V: the action space (Tag: 1 x 5
 // discrete, 2 x 3 continuous).
 template <int KP, int C, int V>
-__global__ void __launch_bounds__(kBfThreads, 6) policy_bf16_kernel(const uint8_t* __restrict__ image, Bf16Args a) {
+#ifndef WDG_BF16_MIN_BLOCKS
+#define WDG_BF16_MIN_BLOCKS 6
+#endif
+__global__ void __launch_bounds__(kBfThreads, WDG_BF16_MIN_BLOCKS) policy_bf16_kernel(const uint8_t* __restrict__ image, Bf16Args a) {
   extern __shared__ __align__(128) uint8_t smb[];
   constexpr int KC1 = KP / 8;  // 16-B chunks per layer-1 row
   const int tid = threadIdx.x, warp = tid >> 5;
