@@ -73,7 +73,9 @@ std::vector<std::string> tag_zero_on_reset() {  // tag_env.cpp:343-346
 // ---- kernel geometry ------------------------------------------------------
 namespace {
 constexpr int kNumSMs = 148;
-constexpr int kBruteMaxAgents = 64;  // brute-force K-NN/resolve below this
+constexpr int kBruteMaxAgents = 64;    // brute-force K-NN/resolve up to this (full obs)
+constexpr int kBruteMaxPartialDisc = 192;  // ... partial obs, discrete without lattice cells
+constexpr int kBruteMaxPartialCont = 160;  // ... partial obs, continuous
 constexpr int kMaxSmem = 227 * 1024;
 
 int32_t round_up(int64_t v, int64_t m) { return static_cast<int32_t>((v + m - 1) / m * m); }
@@ -125,7 +127,25 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   p.placement_h0 = host_mix64(host_substream(cfg.seed, kStreamPlacement));
 
   // Geometry: grid path = one env per CTA; brute path packs envs per CTA.
-  p.use_grid = A > kBruteMaxAgents ? 1 : 0;
+  // Discrete lattice cells (one bucket per grid point) once the grid is at
+  // least half occupied and the cell tables fit: per-cell K-NN lists and
+  // per-cell tagger lookup. Measured at grid 20, 2000 envs, partial K=5:
+  // A = 200 100 vs 151 us/step (gc 14), A = 300 109 vs 166 (gc 17); at
+  // A = 100 it loses (99 vs 76, gc 10).
+  const int64_t g = cfg.grid_size;
+  const int64_t lattice_cell_bytes = 9 + (p.partial ? 4 * (int64_t{p.K} + 1) : 0);
+  const bool lattice_fits = !p.continuous && g <= 128 && g * g <= 2 * A &&
+                            g * g * lattice_cell_bytes <= 96 * 1024;
+  // Partial obs keeps the brute-force K-NN (one env per <= 8 warps) where it
+  // beats the bucket grid at 2000 envs, K=5 (us/step, brute vs grid):
+  // discrete A = 100 58 vs 76, 160 93 vs 140 (ring), 200 139 vs 100 (lattice);
+  // continuous A = 100 79 vs 103, 160 124 vs 167.
+  int brute_max = !p.partial ? kBruteMaxAgents
+                  : p.continuous ? kBruteMaxPartialCont
+                  : lattice_fits ? kBruteMaxAgents : kBruteMaxPartialDisc;
+  if (const char* env = std::getenv("WDG_BRUTE_MAX")) brute_max = std::atoi(env);  // tuning experiments only
+  brute_max = std::min(brute_max, kMaxThreadsPerCta);  // one thread per agent of a packed env
+  p.use_grid = A > brute_max ? 1 : 0;
   if (p.use_grid) {
     // One env per CTA, one thread per agent up to the CTA cap (larger A
     // loops). WDG_TPE_MAX overrides the cap (tuning experiments).
@@ -164,6 +184,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
     p.cell_size = cfg.world_length / p.gc;
   } else {
     p.gc = static_cast<int32_t>(std::min<int64_t>(cfg.grid_size, std::min(sq, 128)));
+    if (lattice_fits) p.gc = static_cast<int32_t>(g);
     if (const char* env = std::getenv("WDG_DISC_GC"))  // tuning experiments only
       p.gc = static_cast<int32_t>(std::clamp<int64_t>(std::atoi(env), 1, std::min<int64_t>(cfg.grid_size, 128)));
     p.lattice_w = static_cast<int32_t>(cfg.grid_size / p.gc);

@@ -498,6 +498,38 @@ struct TopK {
   __device__ __forceinline__ bool admits(float dd, int j) const {
     return dd < wd || (dd == wd && j < wi);
   }
+  // Candidate j above every index already held (ascending scans): ties then
+  // never displace, so the admission and shift tests drop the index compare.
+  __device__ __forceinline__ void consider_next(float dd, int j) {
+    if (!(dd < wd)) return;
+    bool placed = false;
+#pragma unroll
+    for (int t = MAXK - 1; t >= 0; --t) {
+      if (EXACT || t < k) {
+        const bool shift = t > 0 && dd < d[t - 1];
+        if (shift) {
+          d[t] = d[t - 1];
+          i[t] = i[t - 1];
+        } else if (!placed) {
+          d[t] = dd;
+          i[t] = j;
+          placed = true;
+        }
+      }
+    }
+    if (EXACT) {
+      wd = d[MAXK - 1];
+      wi = i[MAXK - 1];
+    } else {
+#pragma unroll
+      for (int t = 0; t < MAXK; ++t) {
+        if (t == k - 1) {
+          wd = d[t];
+          wi = i[t];
+        }
+      }
+    }
+  }
   __device__ __forceinline__ void consider(float dd, int j) {
     if (!admits(dd, j)) return;
     bool placed = false;
@@ -538,7 +570,8 @@ __device__ __forceinline__ float d2_of(float ax, float ay, float bx, float by) {
 
 // Generic ring search over the bucket grid (continuous / non-lattice).
 template <bool CONT, int MAXK, bool EXACT>
-__device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<MAXK, EXACT>& top) {
+__device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<MAXK, EXACT>& top,
+                          bool integral = true) {
   const float sx = s.x[a], sy = s.y[a];
   const int gc = p.gc;
   const int cx = cell_coord<CONT>(sx, p), cy = cell_coord<CONT>(sy, p);
@@ -562,7 +595,8 @@ __device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<M
         const double lb = fmax(0.0, (r - 1) - 1e-3) * cs + edge_in;
         lb2 = static_cast<float>(lb * lb * (1.0 - 1e-5));
       } else {
-        const float lb = static_cast<float>((r - 1) * p.lattice_w + 1);
+        // integral positions sit on their cell's lower edge: one more unit
+        const float lb = static_cast<float>((r - 1) * p.lattice_w + (integral ? 1 : 0));
         lb2 = lb * lb;
       }
       if (top.wd < lb2) break;
@@ -624,23 +658,54 @@ __device__ void knn_lattice(const EnvSmem& s, const TagDevConfig& p, int a, TopK
   knn_rings<false, MAXK, EXACT>(s, p, a, top);
 }
 
+// Brute-force K-NN over integral positions (discrete, d2 < 2^16): each
+// candidate is one 32-bit key (d2 << 16 | j), so the (d2, index) order is an
+// unsigned compare and the top-MAXK insertion is a branchless min/max chain —
+// no divergence when different lanes admit different candidates.
+template <int MAXK>
+__device__ __forceinline__ void knn_brute_keys(const EnvSmem& s, const TagDevConfig& p, int a, int* out) {
+  uint32_t k[MAXK];
+#pragma unroll
+  for (int t = 0; t < MAXK; ++t) k[t] = 0xffffffffu;
+  const float sx = s.x[a], sy = s.y[a];
+  auto put = [&](int j) {
+    const float dx = __fsub_rn(s.x[j], sx), dy = __fsub_rn(s.y[j], sy);
+    const float d2 = __fmaf_rn(dx, dx, __fmul_rn(dy, dy));  // exact: integers below 2^16
+    // 2^23 + d2 holds d2 in its low mantissa bits
+    uint32_t key = __byte_perm(static_cast<uint32_t>(j), __float_as_uint(__fadd_rn(d2, 8388608.0f)), 0x5410);
+#pragma unroll
+    for (int t = 0; t < MAXK; ++t) {
+      const uint32_t lo = min(k[t], key);
+      key = max(k[t], key);
+      k[t] = lo;
+    }
+  };
+  for (int j = 0; j < a; ++j) put(j);
+  for (int j = a + 1; j < p.A; ++j) put(j);
+#pragma unroll
+  for (int t = 0; t < MAXK; ++t) out[t] = static_cast<int>(k[t] & 0xffffu);
+}
+
 template <bool CONT, bool GRID, int MAXK, bool EXACT>
 __device__ __forceinline__ void knn_agent(const EnvSmem& s, const TagDevConfig& p, int a,
-                                          bool lattice_ok, TopK<MAXK, EXACT>& top) {
+                                          bool lattice_ok, TopK<MAXK, EXACT>& top, bool keys_ok = false,
+                                          bool integral = true) {
+  if (!CONT && !GRID && MAXK <= 8 && keys_ok) {
+    knn_brute_keys<MAXK>(s, p, a, top.i);
+    return;
+  }
   top.init(p.K);
   if (!GRID) {
     const float sx = s.x[a], sy = s.y[a];
-    for (int j = 0; j < p.A; ++j) {
-      if (j == a) continue;
-      top.consider(d2_of(sx, sy, s.x[j], s.y[j]), j);
-    }
+    for (int j = 0; j < a; ++j) top.consider_next(d2_of(sx, sy, s.x[j], s.y[j]), j);
+    for (int j = a + 1; j < p.A; ++j) top.consider_next(d2_of(sx, sy, s.x[j], s.y[j]), j);
     return;
   }
   if (!CONT && lattice_ok) {
     knn_lattice<MAXK, EXACT>(s, p, a, top);
     return;
   }
-  knn_rings<CONT, MAXK, EXACT>(s, p, a, top);
+  knn_rings<CONT, MAXK, EXACT>(s, p, a, top, integral);
 }
 
 // Tag resolution for one active runner: resolve kernel (tag_env.cpp:403-456)
@@ -669,7 +734,14 @@ __device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn, bool
     }
   };
   if (!GRID) {
-    for (int j = 0; j < p.A; ++j) consider(j);
+    const int jn = tag_prefix ? p.T : p.A;  // taggers are exactly [0, T)
+    if (exact_cell) {
+      // ascending scan: the first tagger at the runner's cell is the lowest index
+      for (int j = 0; j < jn; ++j)
+        if (s.tag[j] && s.x[j] == rx && s.y[j] == ry) return j;
+      return -1;
+    }
+    for (int j = 0; j < jn; ++j) consider(j);
     return best;
   }
   if (exact_cell) {
@@ -1190,6 +1262,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   const bool first = it == 0;
   // Phase 0: stage the env's agent state in shared memory.
   bool integral = true;
+  bool tprefix = true;
   bool nonfinite = false;
   const bool vec_step = live && vec4 && mode != kModeReinit;
   if (vec_step) {
@@ -1457,6 +1530,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       }
       if (first) s.tag[a] = g.is_tagger[ga + a];
       if (CONT) integral &= (s.tag[a] != 0) == (a < p.T);
+      if (!CONT && !GRID) tprefix &= (s.tag[a] != 0) == (a < p.T);
       s.cred[a] = 0;
       s.tagged[a] = 0;
     }
@@ -1479,6 +1553,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   }
   // CTA-wide AND of `integral` (only read when GRID, i.e. one env per CTA).
   const bool all_integral = __syncthreads_and(integral) != 0;
+  // packed discrete envs: taggers exactly the prefix [0, T) in every env of the CTA
+  const bool all_prefix = (!CONT && !GRID) ? __syncthreads_and(tprefix) != 0 : false;
   if (!CONT && GRID && !all_integral && lt == 0) sc.lattice_ok = 0;
 
   bool reset_now = false;
@@ -1500,7 +1576,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       const int a = base + lt;
       const bool valid = live && a < A;
       const bool runner = valid && !s.tag[a] && s.act[a];
-      const int best = runner ? find_tagger<CONT, GRID>(s, p, a, cell_tagger, CONT && all_integral) : -1;
+      const int best = runner ? find_tagger<CONT, GRID>(s, p, a, cell_tagger, CONT ? all_integral : all_prefix) : -1;
       if (best >= 0) {
         s.act[a] = 0;
         s.tagged[a] = 1;
@@ -1624,11 +1700,15 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         }
       }
       double* es = L.env_stats + e * 8;
-      const bool pre = !GRID && first;  // the prefetched slots are current only on the first step
+      // packed envs: slots [0], [1], [5], [6] stay in registers across the
+      // steps of a multi-step launch (prefetched before the first step)
+      const bool pre = !GRID;
       const double run_t = (pre ? pre_es[0] : es[0]) + st;
       const double run_r = (pre ? pre_es[1] : es[1]) + sr;
-      es[5] = (pre ? pre_es[2] : es[5]) + sc.tags;
-      es[6] = (pre ? pre_es[3] : es[6]) + 1.0;
+      const double es5 = (pre ? pre_es[2] : es[5]) + sc.tags;
+      const double es6 = (pre ? pre_es[3] : es[6]) + 1.0;
+      es[5] = es5;
+      es[6] = es6;
       if (sc.done) {
         es[2] += 1.0;
         es[3] += run_t;
@@ -1638,6 +1718,12 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       } else {
         es[0] = run_t;
         es[1] = run_r;
+      }
+      if (!GRID) {  // one-env CTAs reload them (8 more live registers cost spills there)
+        pre_es[0] = sc.done ? 0.0 : run_t;
+        pre_es[1] = sc.done ? 0.0 : run_r;
+        pre_es[2] = es5;
+        pre_es[3] = es6;
       }
     }
   }
@@ -1704,6 +1790,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   }
   if (!early_inputs) __syncthreads();
   const bool lattice_ok = !CONT && GRID && p.lattice && scal[0].lattice_ok;
+  // packed discrete envs with integral positions (moves and placement keep
+  // them integral): 32-bit-key brute K-NN, d2 <= 2 * 181^2 < 2^16
+  const bool brute_keys = !CONT && !GRID && all_integral && p.world_hi <= 181.0f;
+  // discrete positions all integral (tightens the ring-search bound)
+  const bool disc_integral = !CONT && (GRID ? scal[0].lattice_ok != 0 : all_integral);
 
   // Phase 7: K-NN + observation rows (write_obs_row, tag_env.cpp:165-212).
   const int64_t cta_env0 = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
@@ -1770,7 +1861,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           }
         } else if (PARTIAL && s.act[a]) {
           TopK<MAXK, EXACT> top;
-          knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top);
+          knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top, brute_keys, disc_integral);
           write_row<CONT, (EXACT ? MAXK : 0)>(s, p, sc.step_count, a, row, [&](int n) {
             int j = top.i[0];
 #pragma unroll
@@ -1813,7 +1904,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       for (int a = lt; a < A; a += tpe) {
         if (!s.act[a]) continue;
         TopK<MAXK, EXACT> top;
-        knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top);
+        knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top, brute_keys, disc_integral);
 #pragma unroll
         for (int t = 0; t < MAXK; ++t) {
           if (t < p.K) s.knn[a * p.K + t] = static_cast<uint16_t>(top.i[t]);

@@ -71,6 +71,15 @@ CONFIGS = {
                                  grid_size=7, seed=8), 2),
     "disc_part_9x33_k20": (dict(num_taggers=3, num_runners=30, obs_mode=O.PARTIAL, k_nearest=20,
                                 grid_size=50, seed=9), 9),
+    # C3's A = 100 shape: brute-force K-NN (partial obs up to 128 agents)
+    "disc_part_6x100": (dict(num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, episode_length=50,
+                             seed=10), 6),
+    # brute-force K-NN at 150 agents (grid less than half occupied)
+    "disc_part_4x150": (dict(num_taggers=30, num_runners=120, obs_mode=O.PARTIAL, episode_length=50,
+                             seed=11), 4),
+    # 250 agents on a 30 x 30 grid: ring search over 15 x 15 bucket cells
+    "disc_part_3x250_ring": (dict(num_taggers=50, num_runners=200, obs_mode=O.PARTIAL, grid_size=30,
+                                  episode_length=50, seed=12), 3),
 }
 CONT_CONFIGS = {
     "cont_full_20x12": (dict(variant=O.CONTINUOUS, num_taggers=2, num_runners=10, episode_length=40,
@@ -79,6 +88,8 @@ CONT_CONFIGS = {
                              episode_length=40, world_length=8.0, seed=4), 20),
     "cont_part_3x300": (dict(variant=O.CONTINUOUS, num_taggers=60, num_runners=240, obs_mode=O.PARTIAL,
                              world_length=12.0, tag_radius=0.6, seed=5), 3),
+    "cont_part_5x100": (dict(variant=O.CONTINUOUS, num_taggers=20, num_runners=80, obs_mode=O.PARTIAL,
+                             world_length=10.0, tag_radius=0.5, seed=6), 5),
 }
 
 
@@ -492,3 +503,34 @@ def test_graph_replay_equals_direct_launches(kw, envs):
     np.testing.assert_array_equal(d1.stats()[:5], o.stats()[:5])
     ws1.close()
     ws2.close()
+
+
+@pytest.mark.parametrize("kw,envs", [
+    (dict(num_taggers=3, num_runners=20, obs_mode=O.PARTIAL, seed=31), 9),    # packed brute K-NN
+    (dict(num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, seed=32), 4),   # one-env brute
+    (dict(num_taggers=40, num_runners=160, obs_mode=O.PARTIAL, seed=33), 3),  # lattice cells
+    (dict(num_taggers=20, num_runners=80, seed=34), 4),                        # full obs, grid resolve
+])
+def test_off_lattice_state_falls_back_exactly(kw, envs):
+    """Pushed state outside what placement produces — half-integer positions
+    in some envs, a tagger flag moved off the [0, T) prefix — must disable the
+    integral fast paths (32-bit-key K-NN, lattice cells, prefix resolve) for
+    exactly those steps and stay bit-exact with the oracle."""
+    dc, oc = cfg_pair(**kw)
+    ws = W.Workspace(dc, envs)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, oc.seed)
+    o = O.OracleWorld(oc, envs)
+    A = dc.num_agents()
+    x = o.pull("loc_x").reshape(envs, A)
+    x[0, ::3] += 0.5
+    o.push("loc_x", x)
+    ws.store.push("loc_x", x)
+    tg = o.pull("is_tagger").reshape(envs, A)
+    tg[envs - 1, A - 1] = 1  # a tagger outside the prefix
+    o.push("is_tagger", tg)
+    ws.store.push("is_tagger", tg)
+    for t in range(12):
+        drv.step()
+        o.rollout(t, 1, oc.seed)
+        assert_same(dev_snapshot(ws, o.layout), o.snapshot(), f"off-lattice step {t}")
+    ws.close()
