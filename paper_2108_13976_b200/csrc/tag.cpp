@@ -75,7 +75,7 @@ namespace {
 constexpr int kNumSMs = 148;
 constexpr int kBruteMaxAgents = 64;    // brute-force K-NN/resolve up to this (full obs)
 constexpr int kBruteMaxPartialDisc = 192;  // ... partial obs, discrete without lattice cells
-constexpr int kBruteMaxPartialCont = 160;  // ... partial obs, continuous
+constexpr int kBruteMaxPartialCont = 256;  // ... partial obs, continuous
 constexpr int kMaxSmem = 227 * 1024;
 
 int32_t round_up(int64_t v, int64_t m) { return static_cast<int32_t>((v + m - 1) / m * m); }
@@ -138,8 +138,8 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
                             g * g * lattice_cell_bytes <= 96 * 1024;
   // Partial obs keeps the brute-force K-NN (one env per <= 8 warps) where it
   // beats the bucket grid at 2000 envs, K=5 (us/step, brute vs grid):
-  // discrete A = 100 58 vs 76, 160 93 vs 140 (ring), 200 139 vs 100 (lattice);
-  // continuous A = 100 79 vs 103, 160 124 vs 167.
+  // discrete A = 100 41 vs 76, 160 63 vs 140 (ring), 256 121 vs 99 (lattice);
+  // continuous A = 100 63 vs 103, 200 148 vs 192, 256 185 vs 196.
   int brute_max = !p.partial ? kBruteMaxAgents
                   : p.continuous ? kBruteMaxPartialCont
                   : lattice_fits ? kBruteMaxAgents : kBruteMaxPartialDisc;
@@ -166,8 +166,11 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
       else break;
     }
     p.envs_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (32 * w) / A));
-    p.threads_per_env = p.A;
     p.threads = round_up(static_cast<int64_t>(p.envs_per_cta) * A, 32);
+    // A one-env CTA owns all its threads (the kernel's single-env paths take
+    // every thread as the env's: CTA-uniform barriers and lane-0 updates);
+    // packed CTAs give each env A threads and leave the tail idle.
+    p.threads_per_env = p.envs_per_cta == 1 ? p.threads : p.A;
   }
   p.grid_ctas = static_cast<int32_t>((store.num_envs() + p.envs_per_cta - 1) / p.envs_per_cta);
 

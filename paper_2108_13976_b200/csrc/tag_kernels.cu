@@ -686,12 +686,47 @@ __device__ __forceinline__ void knn_brute_keys(const EnvSmem& s, const TagDevCon
   for (int t = 0; t < MAXK; ++t) out[t] = static_cast<int>(k[t] & 0xffffu);
 }
 
+// Brute-force K-NN, any positions: ascending candidates, so (d2, index)
+// order is a strict d2 compare (ties keep the earlier index). The insertion
+// is a branchless shift: slots from the candidate's rank down move by one.
+// (A compare-exchange chain would be wrong here: a displaced entry must
+// displace its equal-d2 successor, the new candidate must not.)
+template <int MAXK>
+__device__ __forceinline__ void knn_brute_pairs(const EnvSmem& s, const TagDevConfig& p, int a, int* out) {
+  float d[MAXK];
+#pragma unroll
+  for (int t = 0; t < MAXK; ++t) {
+    d[t] = __int_as_float(0x7f800000);
+    out[t] = 0x7fffffff;
+  }
+  const float sx = s.x[a], sy = s.y[a];
+  auto put = [&](int j) {
+    const float dd = d2_of(sx, sy, s.x[j], s.y[j]);
+    bool c[MAXK];
+#pragma unroll
+    for (int t = 0; t < MAXK; ++t) c[t] = dd < d[t];  // monotone in t (d sorted)
+#pragma unroll
+    for (int t = MAXK - 1; t >= 0; --t) {
+      const bool from_prev = t > 0 && c[t > 0 ? t - 1 : 0];
+      const float nd = from_prev ? d[t > 0 ? t - 1 : 0] : dd;
+      const int ni = from_prev ? out[t > 0 ? t - 1 : 0] : j;
+      d[t] = c[t] ? nd : d[t];
+      out[t] = c[t] ? ni : out[t];
+    }
+  };
+  for (int j = 0; j < a; ++j) put(j);
+  for (int j = a + 1; j < p.A; ++j) put(j);
+}
+
 template <bool CONT, bool GRID, int MAXK, bool EXACT>
 __device__ __forceinline__ void knn_agent(const EnvSmem& s, const TagDevConfig& p, int a,
                                           bool lattice_ok, TopK<MAXK, EXACT>& top, bool keys_ok = false,
                                           bool integral = true) {
-  if (!CONT && !GRID && MAXK <= 8 && keys_ok) {
-    knn_brute_keys<MAXK>(s, p, a, top.i);
+  if (!GRID && MAXK <= 8) {
+    if (!CONT && keys_ok)
+      knn_brute_keys<MAXK>(s, p, a, top.i);
+    else
+      knn_brute_pairs<MAXK>(s, p, a, top.i);
     return;
   }
   top.init(p.K);

@@ -44,6 +44,11 @@ CONT = {
                              episode_length=40, world_length=8.0, seed=4), 20),
     "cont_part_3x300": (dict(variant=O.CONTINUOUS, num_taggers=60, num_runners=240, obs_mode=O.PARTIAL,
                              world_length=12.0, tag_radius=0.6, seed=5), 3),
+    # brute-force K-NN: two envs per CTA, and one env per CTA with idle lanes
+    "cont_part_5x100": (dict(variant=O.CONTINUOUS, num_taggers=20, num_runners=80, obs_mode=O.PARTIAL,
+                             episode_length=30, world_length=10.0, tag_radius=0.5, seed=6), 5),
+    "cont_part_2x200": (dict(variant=O.CONTINUOUS, num_taggers=40, num_runners=160, obs_mode=O.PARTIAL,
+                             episode_length=30, world_length=14.0, tag_radius=0.5, seed=7), 2),
 }
 
 
@@ -76,3 +81,28 @@ def test_continuous_free_running_bit_exact(name):
         assert d is None, f"{name} step {t}: first divergence {d}"
     drv.check()
     ws.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cont_full_20x12", "cont_part_5x100", "cont_part_2x200", "cont_part_3x300"])
+def test_continuous_multistep_equals_single_steps(name):
+    """RolloutDriver::run keeps up to 64 steps resident in one launch; with
+    resets inside the window it must equal one launch per step bit-for-bit."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    kw, envs = CONT[name]
+    oc = O.make_config(**kw)
+    dc = W.TagConfig(**{f: getattr(oc, f) for f, _ in O.TagConfigC._fields_})
+    ws1, ws2 = W.Workspace(dc, envs), W.Workspace(dc, envs)
+    d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 9)
+    d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 9)
+    d1.run(70)
+    for _ in range(70):
+        d2.step()
+    names = list(O.array_layout(oc, envs).keys())
+    d = O.first_divergence({n: ws1.store.pull(n) for n in names}, {n: ws2.store.pull(n) for n in names})
+    assert d is None, f"{name}: run(70) vs 70 steps, first divergence {d}"
+    np.testing.assert_array_equal(d1.stats(), d2.stats())
+    ws1.close()
+    ws2.close()

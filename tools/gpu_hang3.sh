@@ -1,0 +1,15 @@
+#!/bin/bash
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+export WDG_BRUTE_MAX=256
+timeout 300 python - <<PY
+import sys, os, time
+sys.path.insert(0, os.getcwd())
+from tools.sweep import measure
+import paper_2108_13976_b200 as W
+for var in (W.CONTINUOUS, W.DISCRETE):
+  for A in (164, 200, 256):
+    T = round(A / 5)
+    cfg = W.TagConfig(variant=var, num_taggers=T, num_runners=A - T, obs_mode=W.PARTIAL, k_nearest=5)
+    sps, ms, geo = measure(cfg, 2000, 200, warmup=3)
+    print("bm=256 var=%d A=%d partial: %.2fM env-steps/s %.1f us/step thr=%d grid=%d" % (var, A, sps / 1e6, ms * 1e3, geo['threads_per_cta'], geo['uses_grid']), flush=True)
+PY

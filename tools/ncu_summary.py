@@ -4,7 +4,8 @@
 
 Writes profiles/<tag>.md (speed-of-light, occupancy, stall reasons, DRAM
 traffic vs algorithmic bytes) and merges {config: dram bytes per launch} into
-profiles/ncu_traffic.json, which bench.py reports as roofline.traffic."""
+profiles/ncu_traffic.json (only with --config NAME, e.g. c2_fused), which
+bench.py reports as roofline.traffic."""
 import csv
 import json
 import os
@@ -68,7 +69,7 @@ def main():
     rep, tag = sys.argv[1], sys.argv[2]
     if "--kernel" in sys.argv:
         KERNEL = sys.argv[sys.argv.index("--kernel") + 1]
-    cfg = "c2_fused"
+    cfg = None  # roofline.traffic entry to update (e.g. c2_fused); none by default
     if "--config" in sys.argv:
         cfg = sys.argv[sys.argv.index("--config") + 1]
     steps = 1
@@ -115,7 +116,7 @@ def main():
     os.makedirs(PROF, exist_ok=True)
     with open(os.path.join(PROF, f"{tag}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    if traffic is not None:
+    if traffic is not None and cfg:
         p = os.path.join(PROF, "ncu_traffic.json")
         cur = {}
         if os.path.exists(p):
