@@ -889,7 +889,7 @@ void Rollout::run(int64_t steps) {
   // steps) consecutive steps are independent launches of the same kernel on
   // the same env, so one launch runs up to kMultiSteps of them with each
   // env's state kept in shared memory (TagLaunch::n_steps).
-  static const bool multi_off = std::getenv("WDG_NO_MULTISTEP") != nullptr;
+  const bool multi_off = std::getenv("WDG_NO_MULTISTEP") != nullptr;  // read per run() (A/B timing in one process)
   if (!multi_off && fused_ok() && pol_[0] == nullptr && steps > 1 && plan_.multistep_ok()) {
     while (steps > 0) {
       const int32_t k = static_cast<int32_t>(std::min<int64_t>(steps, kMultiSteps));

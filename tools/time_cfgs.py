@@ -1,0 +1,23 @@
+"""Device-timed env-steps/s for a few Tag shapes (single-step launches and
+run() windows): python tools/time_cfgs.py [shape ...]   shapes: name=var,A,K,envs"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from tools.sweep import measure  # noqa: E402
+import paper_2108_13976_b200 as W  # noqa: E402
+
+SHAPES = {
+    "c2": (W.DISCRETE, 1000, 5, 2000), "d500": (W.DISCRETE, 500, 5, 2000), "d100": (W.DISCRETE, 100, 5, 2000),
+    "c1000": (W.CONTINUOUS, 1000, 5, 2000), "c300": (W.CONTINUOUS, 300, 5, 2000),
+    "c100": (W.CONTINUOUS, 100, 5, 2000),
+}
+for name in (sys.argv[1:] or list(SHAPES)):
+    var, A, K, E = SHAPES[name]
+    T = round(A / 5)
+    cfg = W.TagConfig(variant=var, num_taggers=T, num_runners=A - T, obs_mode=W.PARTIAL, k_nearest=K)
+    os.environ["WDG_NO_MULTISTEP"] = "1"
+    sps1, ms1, _ = measure(cfg, E, 200, warmup=5)
+    del os.environ["WDG_NO_MULTISTEP"]
+    sps2, ms2, _ = measure(cfg, E, 200, warmup=5)
+    print(f"{name}: single {ms1 * 1e3:.1f} us/step ({sps1 / 1e6:.2f}M)  run {ms2 * 1e3:.1f} us/step ({sps2 / 1e6:.2f}M)", flush=True)
