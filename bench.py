@@ -387,7 +387,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--stats-every", type=int, default=100)
     ap.add_argument("--e2e-steps", type=int, default=200)
-    ap.add_argument("--cpu-steps", type=int, default=1500)
+    ap.add_argument("--cpu-steps", type=int, default=12000)  # ~10 s of reference CPU work at C2
     ap.add_argument("--ref-envs-per-thread", type=int, default=4)
     ap.add_argument("--ref-inner", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
