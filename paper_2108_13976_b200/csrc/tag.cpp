@@ -82,7 +82,34 @@ int32_t round_up(int64_t v, int64_t m) { return static_cast<int32_t>((v + m - 1)
 int32_t align16(int64_t v) { return round_up(v, 16); }
 }  // namespace
 
+namespace {
+TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& cfg, int stage_rows);
+
+int resident_ctas(const TagDevConfig& p) {
+  uint32_t per_sm = 0;
+  TagLaunch q;
+  q.mode = -1;  // occupancy query
+  q.error = &per_sm;
+  return launch_tag_kernel(p, TagDevArrays{}, q, nullptr) == cudaSuccess ? static_cast<int>(per_sm) : 0;
+}
+}  // namespace
+
+// Wide continuous rows (K=5, D=41) may stage half a warp's rows per pass
+// (TagDevConfig::stage_rows = 16); that costs a second pass per warp, so it is
+// taken only when the smaller CTA fits more CTAs per SM. Measured at 2000
+// envs: A = 1000 491 -> 473 us/step (2 -> 3 CTAs per SM); A = 300, where the
+// register cap already holds it at 3, 265 -> 285 us/step.
 TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) {
+  TagDevConfig full = make_dev_config_rows(store, cfg, 32);
+  if (!full.continuous || !full.partial || full.K != 5 || !full.use_grid || !full.stage_obs) return full;
+  if (std::getenv("WDG_STAGE_FULL_WARP") != nullptr) return full;
+  TagDevConfig half = make_dev_config_rows(store, cfg, 16);
+  if (std::getenv("WDG_STAGE_HALF_WARP") != nullptr) return half;  // tuning experiments only
+  return resident_ctas(half) > resident_ctas(full) ? half : full;
+}
+
+namespace {
+TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& cfg, int stage_rows) {
   validate_tag_config(cfg);
   TagDevConfig p;
   const int64_t A = cfg.num_taggers + cfg.num_runners;
@@ -196,10 +223,17 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   p.ncells = p.gc * p.gc;
   // Observation rows staged per warp in shared memory when a row is narrow.
   const int64_t nwarps = p.threads / 32;
-  const int64_t stage_bytes = nwarps * 32 * int64_t{p.D} * 4;
+  int64_t stage_bytes = nwarps * 32 * int64_t{p.D} * 4;
   p.stage_obs = (p.D <= 64 && stage_bytes <= 112 * 1024) ? 1 : 0;
   if (const char* env = std::getenv("WDG_STAGE_OBS")) p.stage_obs = p.stage_obs && std::atoi(env) != 0;
-  p.stage_floats = 32 * p.D;
+  // Continuous K=5 rows (D = 41) at one env per CTA may use half-warp passes
+  // (see make_dev_config): the staging buffer halves (42 -> 21 KB at 256 threads).
+  p.stage_rows = 32;
+  if (stage_rows == 16 && p.continuous && p.partial && p.K == 5 && p.use_grid && p.stage_obs) {
+    p.stage_rows = 16;
+    stage_bytes /= 2;
+  }
+  p.stage_floats = p.stage_rows * p.D;
 
   // Shared-memory carve-up per env.
   int64_t off = 0;
@@ -214,13 +248,19 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   if (p.continuous) {
     p.off_speed = take(4 * A, 16);
     p.off_dir = take(4 * A, 16);
-    p.off_sin = take(4 * A, 16);
-    p.off_cos = take(4 * A, 16);
   }
   p.off_cred = take(4 * A, 16);
   p.off_tag = take(A, 16);
   p.off_act = take(A, 16);
   p.off_tagged = take(A, 16);
+  // Arrays from here on are first written after phase 1 (sin/cos in phase
+  // 4/6, the K-NN lists and the bucket grid from phase 2), so the bulk-copy
+  // logits zone may overlay them.
+  const int64_t late_begin = align16(off);
+  if (p.continuous) {
+    p.off_sin = take(4 * A, 16);
+    p.off_cos = take(4 * A, 16);
+  }
   if (p.partial && !p.stage_obs) p.off_knn = take(2 * A * p.K, 4);
   if (p.use_grid) {
     p.off_cstart = take(4 * (p.ncells + 1), 4);
@@ -240,13 +280,13 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   }
   // Bulk-copy input staging (one env per CTA, A % 4 == 0): the env's f64
   // logits rows land by one TMA bulk copy in a zone that overlays the
-  // bucket-grid and obs-staging areas, which are dead until phase 2. The
-  // zone starts at the grid block (CTA offset head + off_cstart) and grows
+  // late arrays, the bucket grid and the obs staging, dead until phase 2. The
+  // zone starts at the first late array (CTA offset head + late_begin) and grows
   // the CTA's smem if the logits need more than those areas.
   p.bulk_in = 0;
   if (p.use_grid && (A % 4) == 0 && std::getenv("WDG_NO_BULK") == nullptr) {
     const int64_t logits_bytes = int64_t{A} * p.C * p.V * 8;
-    const int64_t zone = align16(static_cast<int64_t>(p.head_bytes) + p.off_cstart);
+    const int64_t zone = align16(static_cast<int64_t>(p.head_bytes) + late_begin);
     const int64_t need = zone + logits_bytes;
     if (std::max<int64_t>(total, need) <= kMaxSmem && logits_bytes % 16 == 0) {
       p.bulk_in = 1;
@@ -267,6 +307,7 @@ TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) 
   p.smem_bytes = static_cast<int32_t>(total);
   return p;
 }
+}  // namespace
 
 TagDevArrays bind_dev_arrays(DataStore& store, const wdg_tag_config& cfg) {
   // bind_arrays (tag_env.cpp:81-124) — same names, device addresses.

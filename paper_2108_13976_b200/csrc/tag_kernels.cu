@@ -1853,6 +1853,69 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       build_cell_lists(s, p, L.ablate);
       __syncthreads();
     }
+    if constexpr (CONT && EXACT && PARTIAL) {
+      if (p.stage_rows == 16) {
+        // Wide continuous rows (D = 41): the K-NN runs on all 32 lanes, then
+        // each half-warp builds and streams its 16 rows through a half-size
+        // staging buffer (smem that buys the CTA a third slot per SM).
+        for (int base = 0; base < A; base += tpe) {
+          const int a = base + lt;
+          const bool valid = live && a < A;
+          const bool act_a = valid && s.act[a];
+          int nb[MAXK];
+          if (act_a && !(L.ablate & 4u)) {
+            TopK<MAXK, EXACT> top;
+            knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, false, top);
+#pragma unroll
+            for (int t = 0; t < MAXK; ++t) nb[t] = top.i[t];
+          }
+          const int myrow = env_ok ? le * A + a : -1;
+          const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const bool mine = valid && (lane >> 4) == h;
+            if (mine) {
+              float* row = stage + (lane & 15) * D;
+              if (L.ablate & 4u) {
+                row[0] = static_cast<float>(a);
+              } else if (!act_a) {
+                constexpr int kD = MAXK * 7 + 5 + 1;
+#pragma unroll
+                for (int f = 0; f < kD; ++f) row[f] = 0.0f;
+              } else {
+                write_row<CONT, MAXK>(s, p, sc.step_count, a, row, [&](int n) {
+                  int j = nb[0];
+#pragma unroll
+                  for (int t = 1; t < MAXK; ++t)
+                    if (t == n) j = nb[t];
+                  return j;
+                });
+              }
+            }
+            __syncwarp();
+            const unsigned hm = (vmask >> (16 * h)) & 0xffffu;
+            const int row0 = __shfl_sync(0xffffffffu, myrow, 16 * h);
+            if (hm != 0u && (hm & (hm + 1u)) == 0u) {
+              const int nf = __popc(hm) * D;
+              float* dst = cta_out + static_cast<int64_t>(row0) * D;
+              if (vec && ((static_cast<int64_t>(row0) * D) & 3) == 0) {
+                const int nv = nf >> 2;
+                for (int v = lane; v < nv; v += 32)
+                  __stcs(reinterpret_cast<float4*>(dst) + v, reinterpret_cast<const float4*>(stage)[v]);
+                for (int f = (nv << 2) + lane; f < nf; f += 32) __stcs(dst + f, stage[f]);
+              } else {
+                for (int f = lane; f < nf; f += 32) __stcs(dst + f, stage[f]);
+              }
+            } else if (mine) {
+              float* dst = cta_out + static_cast<int64_t>(myrow) * D;
+              for (int f = 0; f < D; ++f) __stcs(dst + f, stage[(lane & 15) * D + f]);
+            }
+            __syncwarp();
+          }
+        }
+        goto obs_done;
+      }
+    }
     for (int base = 0; base < A; base += tpe) {
       const int a = base + lt;
       const bool valid = live && a < A;

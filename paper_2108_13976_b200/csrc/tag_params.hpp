@@ -77,7 +77,8 @@ struct TagDevConfig {
   int32_t lattice = 0;            // discrete with one grid cell per lattice point
   int32_t stage_obs = 0;          // per-warp smem staging of observation rows
   int32_t off_stage = 0;          // CTA offset of the staging area
-  int32_t stage_floats = 0;       // floats per warp staging buffer (32 * D)
+  int32_t stage_floats = 0;       // floats per warp staging buffer (stage_rows * D)
+  int32_t stage_rows = 32;        // rows staged per warp pass (16: wide continuous rows)
   int32_t gc = 1, ncells = 1;     // grid cells per side / total
   int32_t lattice_w = 1;          // discrete: floor(grid_size / gc)
   float cell_inv = 1.f;           // continuous: gc / world_length

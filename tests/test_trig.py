@@ -106,3 +106,40 @@ def test_continuous_multistep_equals_single_steps(name):
     np.testing.assert_array_equal(d1.stats(), d2.stats())
     ws1.close()
     ws2.close()
+
+
+@pytest.mark.gpu
+def test_continuous_half_warp_staging_bit_exact(monkeypatch):
+    """Wide continuous rows staged by half-warps (chosen automatically when it
+    fits more CTAs per SM, as at A = 1000; forced here at A = 300): bit-exact."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    if not O.libm_matches_replica():
+        pytest.skip("host libm is not the glibc FMA variant the device replicates")
+    kw, envs = CONT["cont_part_3x300"]
+    oc = O.make_config(**{**kw, "episode_length": 25})
+    dc = W.TagConfig(**{f: getattr(oc, f) for f, _ in O.TagConfigC._fields_})
+    monkeypatch.setenv("WDG_STAGE_HALF_WARP", "1")
+    ws = W.Workspace(dc, envs)
+    monkeypatch.delenv("WDG_STAGE_HALF_WARP")
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, oc.seed)
+    o = O.OracleWorld(oc, envs)
+    for t in range(40):
+        drv.step()
+        o.rollout(t, 1, oc.seed)
+        d = O.first_divergence({n: ws.store.pull(n) for n in o.layout}, o.snapshot())
+        assert d is None, f"half-warp staging step {t}: first divergence {d}"
+    ws2 = W.Workspace(dc, envs)  # multi-step windows on the same plan choice
+    monkeypatch.setenv("WDG_STAGE_HALF_WARP", "1")
+    ws3 = W.Workspace(dc, envs)
+    monkeypatch.delenv("WDG_STAGE_HALF_WARP")
+    d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 4)
+    d3 = W.RolloutDriver(ws3.store, ws3.plan, ws3.resets, 4)
+    d2.run(50)
+    d3.run(50)
+    names = list(o.layout)
+    d = O.first_divergence({n: ws2.store.pull(n) for n in names}, {n: ws3.store.pull(n) for n in names})
+    assert d is None, f"half vs full staging after run(50): first divergence {d}"
+    for w in (ws, ws2, ws3):
+        w.close()
