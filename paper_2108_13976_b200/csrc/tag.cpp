@@ -176,7 +176,15 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   if (p.use_grid) {
     // One env per CTA, one thread per agent up to the CTA cap (larger A
     // loops). WDG_TPE_MAX overrides the cap (tuning experiments).
-    int cap = 256;  // 4 CTAs (envs) per SM overlap each other's barriers (measured best)
+    // Thread cap per env, measured at 2000 envs, partial K=5 (us/step at
+    // 128 / 192 / 256 threads): discrete A = 200 85 / - / 97, 300 86 / - / 102,
+    // 500 89 / - / 104, 700 130 / 112 / 118, 1000 177 / 160 / 136;
+    // continuous A = 300 201 / 218 / 250, 500 298 / 277 / 280, 1000 600 / - / 476.
+    // Smaller envs keep more CTAs (envs) per SM overlapping each other's
+    // barriers; at C2 four 256-thread envs per SM are best.
+    int cap = 256;
+    if (p.partial && (p.continuous ? A <= 400 : A <= 512)) cap = 128;
+    else if (p.partial && !p.continuous && A <= 864) cap = 192;
     if (const char* env = std::getenv("WDG_TPE_MAX")) cap = std::clamp(std::atoi(env), 32, 1024) / 32 * 32;
     cap = std::min(cap, kMaxThreadsPerCta);
     p.envs_per_cta = 1;
@@ -424,6 +432,10 @@ bool TagPlan::multistep_ok() {
     // the wide-row writer is 6-9% slower than the single-step build
     // (profiles/sweep_r01.json), which outweighs the saved state reloads
     if (dev_.use_grid && !dev_.partial) multistep_ = 0;
+    // discrete grid envs below 256 threads (A <= 864): the looped build
+    // measured 3-36% slower than one launch per step (e.g. A = 300: 117 vs
+    // 86 us/step)
+    if (dev_.use_grid && !dev_.continuous && dev_.threads < 256) multistep_ = 0;
     if (dev_.use_grid && dev_.partial && !dev_.lattice) {
       uint32_t per_sm = 0;
       TagLaunch q;

@@ -11,6 +11,8 @@ SHAPES = {
     "c2": (W.DISCRETE, 1000, 5, 2000), "d500": (W.DISCRETE, 500, 5, 2000), "d100": (W.DISCRETE, 100, 5, 2000),
     "c1000": (W.CONTINUOUS, 1000, 5, 2000), "c300": (W.CONTINUOUS, 300, 5, 2000),
     "c100": (W.CONTINUOUS, 100, 5, 2000),
+    "d200": (W.DISCRETE, 200, 5, 2000), "d300": (W.DISCRETE, 300, 5, 2000), "d700": (W.DISCRETE, 700, 5, 2000),
+    "c500": (W.CONTINUOUS, 500, 5, 2000),
 }
 for name in (sys.argv[1:] or list(SHAPES)):
     var, A, K, E = SHAPES[name]
