@@ -77,6 +77,9 @@ CONFIGS = {
     # brute-force K-NN at 150 agents (grid less than half occupied)
     "disc_part_4x150": (dict(num_taggers=30, num_runners=120, obs_mode=O.PARTIAL, episode_length=50,
                              seed=11), 4),
+    # 3000 agents on a 40 x 40 lattice (12 agent strides per thread, 1600 cells)
+    "disc_part_2x3000_g40": (dict(num_taggers=600, num_runners=2400, obs_mode=O.PARTIAL, grid_size=40,
+                                  episode_length=20, seed=13), 2),
     # 250 agents on a 30 x 30 grid: ring search over 15 x 15 bucket cells
     "disc_part_3x250_ring": (dict(num_taggers=50, num_runners=200, obs_mode=O.PARTIAL, grid_size=30,
                                   episode_length=50, seed=12), 3),
