@@ -249,46 +249,6 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return y;
 }
 
-// tanh on the FMA/ALU pipes (the MUFU unit that runs tanh.approx is the bf16
-// forward's bottleneck: 128 activations per row): 16 cubic pieces on [0, 4)
-// (max |error| 9.2e-6, far below bf16's 2^-9), tanh = 1 beyond (error 6.7e-4
-// at 4), odd symmetry. The interval index comes from a float add (no F2I on
-// the conversion unit); the coefficients are one 16-B shared-memory load.
-__constant__ float4 c_tanh_pieces[16] = {
-    {-3.885739229e-06f, 1.000295560e+00f, -4.763446850e-03f, -3.109364195e-01f},
-    {2.449095924e-01f, 9.407441267e-01f, -2.432355171e-01f, -1.782694943e-01f},
-    {4.621094067e-01f, 7.870826791e-01f, -3.751189573e-01f, -1.878590100e-02f},
-    {6.351453709e-01f, 5.968849915e-01f, -3.846054834e-01f, 8.078340436e-02f},
-    {7.615938288e-01f, 4.200062380e-01f, -3.205932881e-01f, 1.104158206e-01f},
-    {8.482847620e-01f, 2.803258317e-01f, -2.363196785e-01f, 9.940529010e-02f},
-    {9.051496392e-01f, 1.805944190e-01f, -1.615383631e-01f, 7.518830769e-02f},
-    {9.413767018e-01f, 1.137172712e-01f, -1.054074783e-01f, 5.188201017e-02f},
-    {9.640284211e-01f, 7.058206307e-02f, -6.684665007e-02f, 3.397764245e-02f},
-    {9.780266788e-01f, 4.341872873e-02f, -4.165931125e-02f, 2.157967033e-02f},
-    {9.866146611e-01f, 2.656247926e-02f, -2.568767623e-02f, 1.345719071e-02f},
-    {9.918599526e-01f, 1.619558800e-02f, -1.573714857e-02f, 8.300309055e-03f},
-    {9.950548949e-01f, 9.854450091e-03f, -9.603253972e-03f, 5.085780841e-03f},
-    {9.969977223e-01f, 5.988595553e-03f, -5.846190576e-03f, 3.103717853e-03f},
-    {9.981779506e-01f, 3.636532826e-03f, -3.553837431e-03f, 1.889532320e-03f},
-    {9.988944750e-01f, 2.207240238e-03f, -2.158439442e-03f, 1.148652898e-03f}};
-__device__ __forceinline__ float tanh_poly(float x, const float4* pieces) {
-  const float ax = fminf(fabsf(x), 3.9999998f);
-  // 2^23 + 4|x| rounded DOWN: floor(4|x|) lands in the low mantissa bits
-  const float q = __fadd_rd(__fmul_rn(ax, 4.0f), 8388608.0f);
-  const int k = __float_as_int(q) & 15;
-  const float u = __fsub_rn(ax, __fmul_rn(__fsub_rn(q, 8388608.0f), 0.25f));  // exact floor, no I2F
-  const float4 c = pieces[k];
-  float y = __fmaf_rn(__fmaf_rn(__fmaf_rn(c.w, u, c.z), u, c.y), u, c.x);
-  y = fabsf(x) >= 4.0f ? 1.0f : y;
-  return copysignf(y, x);
-}
-#ifndef WDG_TANH_POLY_EVERY
-// 1 in N activations on the FMA pipe (0 = all on MUFU). Measured at C2 (rollout
-// ms/step): 0 -> 0.294, 4 -> 0.317, 2 -> 0.368 — the polynomial's registers
-// (spills at the 6-CTA cap) cost more than the MUFU time it saves. Off.
-#define WDG_TANH_POLY_EVERY 0
-#endif
-
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -317,7 +277,7 @@ __host__ __device__ constexpr int bf_image_bytes(int Kp) {
   return 64 * Kp * 2 + 64 * 64 * 2 + 16 * 64 * 2 + (64 + 64 + 16) * 4;
 }
 __host__ __device__ constexpr int bf_smem_bytes(int Kp) {
-  return bf_image_bytes(Kp) + 128 * 64 * 2 + 16 + 16 + 16 * 16;  // + tanh pieces
+  return bf_image_bytes(Kp) + 128 * 64 * 2 + 16 + 16;
 }
 static_assert(bf_image_bytes(16) % 16 == 0 && bf_image_bytes(32) % 16 == 0 && bf_image_bytes(48) % 16 == 0,
               "image size");
@@ -371,9 +331,7 @@ __global__ void __launch_bounds__(kBfThreads, WDG_BF16_MIN_BLOCKS) policy_bf16_k
   uint8_t* As = reinterpret_cast<uint8_t*>(b3s + 16);  // 16-B aligned (image size % 16 == 0)
   uint64_t* bar = reinterpret_cast<uint64_t*>(As + 128 * 64 * 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
-  float4* tanh_pieces = reinterpret_cast<float4*>(tmem_slot + 4);  // 16 x 16 B
   constexpr int W = C * V;
-  if (tid < 16) tanh_pieces[tid] = c_tanh_pieces[tid];
 
   // The weights' smem image (bf16 operand tiles + f32 biases) was packed once
   // on the host (Policy::upload, bf16_image): a straight 16-B copy.
@@ -477,13 +435,7 @@ __global__ void __launch_bounds__(kBfThreads, WDG_BF16_MIN_BLOCKS) policy_bf16_k
           float v[16];
           tmem_ld16(tmem + lane_base + q4 * 16, v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float h = v[i] + bias[q4 * 16 + i];
-            v[i] = (WDG_TANH_POLY_EVERY > 0 && i % (WDG_TANH_POLY_EVERY > 0 ? WDG_TANH_POLY_EVERY : 1) ==
-                                                   (WDG_TANH_POLY_EVERY > 0 ? WDG_TANH_POLY_EVERY : 1) - 1)
-                       ? tanh_poly(h, tanh_pieces)
-                       : tanh_fast(h);
-          }
+          for (int i = 0; i < 16; ++i) v[i] = tanh_fast(v[i] + bias[q4 * 16 + i]);
 #pragma unroll
           for (int c2 = 0; c2 < 2; ++c2) {
             const float* x = v + c2 * 8;
