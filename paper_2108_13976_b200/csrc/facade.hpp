@@ -107,6 +107,13 @@ class DataStore {
   // Scratch owned by the store, reused by reset paths.
   uint8_t* env_mask();
   int64_t* id_buffer(int64_t count);
+  // Per-env sequence flags for programmatic dependent launch of consecutive
+  // fused steps (TagLaunch::env_seq), shared by every rollout on this store.
+  // A launch uses pdl_seq() + 1 and calls commit_pdl_seq() once it is
+  // enqueued, so a failed launch never leaves a sequence number nobody sets.
+  uint32_t* pdl_flags();
+  uint32_t pdl_seq() const noexcept { return pdl_seq_; }
+  void commit_pdl_seq() noexcept { ++pdl_seq_; }
 
  private:
   struct Entry {
@@ -130,6 +137,8 @@ class DataStore {
   int64_t ids_cap_ = 0;
   void* descs_ = nullptr;
   int32_t descs_cap_ = 0;
+  uint32_t* pdl_flags_ = nullptr;
+  uint32_t pdl_seq_ = 0;
   friend class ResetManager;
 };
 
@@ -264,6 +273,7 @@ class Rollout {
   uint32_t* error_ = nullptr;
   int32_t* own_episode_ = nullptr;
   uint64_t h_actions0_ = 0;
+  uint32_t* pdl_flags_ = nullptr;  // the store's (DataStore::pdl_flags)
   // host-driven stepping: double-buffered logits + copy stream
   cudaStream_t copy_ = nullptr;
   double* dlog_[2] = {nullptr, nullptr};

@@ -40,6 +40,17 @@ DataStore::~DataStore() {
   if (mask_) cudaFree(mask_);
   if (ids_) cudaFree(ids_);
   if (descs_) cudaFree(descs_);
+  if (pdl_flags_) cudaFree(pdl_flags_);
+}
+
+uint32_t* DataStore::pdl_flags() {
+  if (pdl_flags_ == nullptr) {
+    const size_t bytes = static_cast<size_t>(num_envs_) * sizeof(uint32_t);
+    cuda_check(cudaMalloc(&pdl_flags_, bytes), "cudaMalloc(pdl flags)");
+    cuda_check(cudaMemset(pdl_flags_, 0, bytes), "memset(pdl flags)");  // before any stream uses them
+    pdl_seq_ = 0;
+  }
+  return pdl_flags_;
 }
 
 void DataStore::set_env_offset(int64_t off) {

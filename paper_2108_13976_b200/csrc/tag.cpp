@@ -641,6 +641,8 @@ Rollout::Rollout(DataStore& store, TagPlan& plan, ResetManager* resets, uint64_t
   }
   logits_ = zero_logits_;
   h_actions0_ = host_mix64(host_substream(seed_, kStreamActions));
+  // WDG_NO_PDL (A/B timing and tests): one plain launch per step
+  if (std::getenv("WDG_NO_PDL") == nullptr) pdl_flags_ = store_.pdl_flags();
 }
 
 Rollout::~Rollout() {
@@ -825,7 +827,21 @@ void Rollout::step_unfused() {
 void Rollout::step() {
   forward_policies(store_.stream(), t_, nullptr, 0, nullptr, false, true);
   if (fused_ok()) {
-    plan_.launch(fused_launch(t_));
+    TagLaunch L = fused_launch(t_);
+    // Consecutive fused steps overlap through programmatic dependent launch
+    // (per-env waits, TagLaunch::env_seq). With device policies every step
+    // is serialised behind the policy kernels anyway.
+    // Not while the stream is being captured into someone's graph: the
+    // sequence numbers would be baked in and replays would not wait.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    const bool capturing = cudaStreamIsCapturing(store_.stream(), &cs) != cudaSuccess ||
+                           cs != cudaStreamCaptureStatusNone;
+    if (pol_[0] == nullptr && !capturing && pdl_flags_ != nullptr) {
+      L.env_seq = pdl_flags_;
+      L.seq = store_.pdl_seq() + 1u;
+    }
+    plan_.launch(L);
+    if (L.env_seq != nullptr) store_.commit_pdl_seq();
     ++launches_;
   } else {
     step_unfused();

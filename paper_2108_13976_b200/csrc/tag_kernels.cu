@@ -1264,6 +1264,28 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     const bool l0 = e0 < p.E && !(mode == kModeReinit && L.env_mask != nullptr && !L.env_mask[e0]);
     if (!l0) return;
   }
+  // Programmatic dependent launch (TagLaunch::env_seq): release the next
+  // launch now, then wait for this CTA's envs' previous step only. ld.acquire
+  // + the barrier order every thread's later loads (generic and, after the
+  // proxy fence, the bulk copies) after that step's writes.
+  const bool pdl = L.env_seq != nullptr;
+  if (pdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (tid == 0) {
+      const int64_t eb = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
+      for (int k = 0; k < p.envs_per_cta && eb + k < p.E; ++k) {
+        const uint32_t* f = L.env_seq + eb + k;
+        uint32_t v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+          if (static_cast<int32_t>(v - (L.seq - 1u)) >= 0) break;
+          __nanosleep(64);
+        }
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+  }
 
   // Per-env scalars are loaded first (by the env's lane 0) so their latency
   // overlaps the per-agent loads instead of following them; packed-env CTAs
@@ -2084,6 +2106,15 @@ obs_done:
   }
   if (n_steps > 1) __syncthreads();  // the next step rewrites the shared state
   }  // multi-step loop
+  if (pdl) {  // publish this CTA's envs to the next launch
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t eb = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
+      for (int k = 0; k < p.envs_per_cta && eb + k < p.E; ++k)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(L.env_seq + eb + k), "r"(L.seq) : "memory");
+    }
+  }
 }
 
 // ---- standalone sampler: sample_actions (sampler.cpp:5-40) ----------------
@@ -2243,6 +2274,19 @@ cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const T
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            p.smem_bytes);
     if (err != cudaSuccess) return err;
+  }
+  if (L.env_seq != nullptr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(p.grid_ctas));
+    cfg.blockDim = dim3(static_cast<unsigned>(p.threads));
+    cfg.dynamicSmemBytes = static_cast<size_t>(p.smem_bytes);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p, g, L);
   }
   kern<<<p.grid_ctas, p.threads, p.smem_bytes, st>>>(p, g, L);
   return cudaGetLastError();

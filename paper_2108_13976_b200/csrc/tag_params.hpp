@@ -130,6 +130,14 @@ struct TagLaunch {
   uint8_t* cap_active = nullptr;
   float* cap_rewards = nullptr;
   uint8_t* cap_done = nullptr;
+  // Programmatic dependent launch between consecutive fused steps
+  // (RolloutDriver::step): env_seq[e] holds the sequence number of the last
+  // launch that finished env e. This launch (sequence `seq`) lets the next one
+  // start as soon as all its CTAs are resident, and each CTA waits only for
+  // its own envs' previous launch (env_seq[e] == seq - 1), so the next step's
+  // early envs run in the current step's tail. nullptr = plain launch.
+  uint32_t* env_seq = nullptr;
+  uint32_t seq = 0;
   // Performance-analysis only (WDG_ABLATE env var, never set by the product,
   // tests or bench): bit0 skip exp/sampling, bit1 skip cell K-NN, bit2 skip
   // obs rows, bit3 skip grid build. Results are WRONG when non-zero.

@@ -537,3 +537,34 @@ def test_off_lattice_state_falls_back_exactly(kw, envs):
         o.rollout(t, 1, oc.seed)
         assert_same(dev_snapshot(ws, o.layout), o.snapshot(), f"off-lattice step {t}")
     ws.close()
+
+
+@pytest.mark.parametrize("kw,envs", [
+    (dict(num_taggers=200, num_runners=800, obs_mode=O.PARTIAL, episode_length=30, seed=41), 1500),
+    (dict(num_taggers=1, num_runners=4, episode_length=9, seed=42), 5000),
+    (dict(variant=O.CONTINUOUS, num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, episode_length=12,
+          seed=43), 1200),
+])
+def test_overlapped_steps_equal_serial_steps(kw, envs, monkeypatch):
+    """RolloutDriver::step launches consecutive fused steps with programmatic
+    dependent launch: a CTA of step t+1 starts once its own envs finished step
+    t, inside step t's tail. 100 back-to-back steps (no host sync, resets
+    included, several waves of CTAs) must equal the same steps launched one
+    after another without overlap (WDG_NO_PDL)."""
+    dc, oc = cfg_pair(**kw)
+    ws1 = W.Workspace(dc, envs)
+    d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 5)
+    monkeypatch.setenv("WDG_NO_PDL", "1")
+    ws2 = W.Workspace(dc, envs)
+    d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 5)
+    monkeypatch.delenv("WDG_NO_PDL")
+    for _ in range(100):
+        d1.step()
+    for _ in range(100):
+        d2.step()
+    names = list(O.array_layout(oc, envs).keys())
+    d = O.first_divergence(dev_snapshot(ws1, names), dev_snapshot(ws2, names))
+    assert d is None, f"overlapped vs serial steps: first divergence {d}"
+    np.testing.assert_array_equal(d1.stats(), d2.stats())
+    ws1.close()
+    ws2.close()

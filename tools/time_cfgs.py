@@ -13,6 +13,8 @@ SHAPES = {
     "c100": (W.CONTINUOUS, 100, 5, 2000),
     "d200": (W.DISCRETE, 200, 5, 2000), "d300": (W.DISCRETE, 300, 5, 2000), "d700": (W.DISCRETE, 700, 5, 2000),
     "c500": (W.CONTINUOUS, 500, 5, 2000),
+    "c2_e1776": (W.DISCRETE, 1000, 5, 1776), "c2_e2368": (W.DISCRETE, 1000, 5, 2368),
+    "c2_e1184": (W.DISCRETE, 1000, 5, 1184), "c2_e4000": (W.DISCRETE, 1000, 5, 4000),
 }
 for name in (sys.argv[1:] or list(SHAPES)):
     var, A, K, E = SHAPES[name]
