@@ -161,6 +161,8 @@ class TagPlan {
   void launch(TagLaunch L);
   // Whether RolloutDriver::run may use multi-step residency launches.
   bool multistep_ok();
+  // Whether consecutive fused launches overlap (programmatic dependent launch).
+  bool pdl_ok() const;
   const wdg_tag_config& config() const { return cfg_; }
   const TagDevConfig& dev() const { return dev_; }
   DataStore& store() { return store_; }
@@ -274,6 +276,8 @@ class Rollout {
   int32_t* own_episode_ = nullptr;
   uint64_t h_actions0_ = 0;
   uint32_t* pdl_flags_ = nullptr;  // the store's (DataStore::pdl_flags)
+  bool graph_pdl_ = false;         // the captured graph's nodes overlap (PDL)
+  void set_pdl(TagLaunch& L) const;
   // host-driven stepping: double-buffered logits + copy stream
   cudaStream_t copy_ = nullptr;
   double* dlog_[2] = {nullptr, nullptr};

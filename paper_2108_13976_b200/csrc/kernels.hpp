@@ -24,7 +24,8 @@ cudaError_t launch_mask_from_done(const uint8_t* done, uint8_t* mask, int64_t E,
 cudaError_t launch_mask_from_ids(const int64_t* ids, int64_t n, uint8_t* mask, cudaStream_t st);
 cudaError_t launch_restore_zero(const ResetRowDesc* descs, int ndesc, const uint8_t* mask,
                                 uint8_t* done, int32_t* episode, int64_t E, cudaStream_t st);
-cudaError_t launch_set_counter(int64_t* ptr, int64_t value, cudaStream_t st);
+// ptr[0] = value; ptr[1] = value2 when value2 >= 0
+cudaError_t launch_set_counter(int64_t* ptr, int64_t value, cudaStream_t st, int64_t value2 = -1);
 cudaError_t launch_stats_reduce(const double* env_stats, int64_t E, double* out, cudaStream_t st);
 
 }  // namespace wdg

@@ -425,6 +425,21 @@ void TagPlan::launch(TagLaunch L) {
 // K-NN (continuous / non-lattice discrete partial obs) at fewer than 3 waves
 // of CTAs, where it measured 2-18% slower, and grid-path full observations
 // (profiles/sweep_r01.json: single_step vs run_multistep).
+// Overlapping consecutive fused launches (TagLaunch::env_seq) measured, per
+// step at 2000 envs (us, overlapped vs serial): C2 127 vs 135, continuous
+// partial A = 1000 449 vs 476 (A = 300 202 vs 203), grid full obs A = 100 61
+// vs 80, brute partial A = 100 37 vs 44 — but discrete partial grids below 256
+// threads lose (A = 200 / 300 / 500 / 700: 106 / 109 / 103 / 117 vs 86 / 87 /
+// 90 / 112) and so do the tiny packed envs of C4 (10.0 vs 8.2; 22.8 vs 8.6
+// at 10000 envs, 25 envs per CTA), where the per-env waits cost more than the
+// few-microsecond kernels can overlap.
+bool TagPlan::pdl_ok() const {
+  if (const char* env = std::getenv("WDG_PDL")) return std::atoi(env) != 0;  // A/B experiments
+  if (!dev_.use_grid) return dev_.envs_per_cta <= 4 && dev_.threads >= 128;
+  if (!dev_.continuous && dev_.partial) return dev_.threads >= 256;
+  return true;
+}
+
 bool TagPlan::multistep_ok() {
   if (multistep_ < 0) {
     multistep_ = 1;
@@ -824,22 +839,27 @@ void Rollout::step_unfused() {
   launches_ += policy_samples() ? 1 : 2;  // (+ the reset kernels, counted in the ResetManager's own launches)
 }
 
+// Consecutive fused launches overlap through programmatic dependent launch
+// (per-env waits, TagLaunch::env_seq). Not with device policies (every step
+// is serialised behind the policy kernels anyway), and not while the stream
+// is being captured into someone's graph: the sequence numbers would be baked
+// in and replays would not wait.
+void Rollout::set_pdl(TagLaunch& L) const {
+  if (pol_[0] != nullptr || pdl_flags_ == nullptr || !plan_.pdl_ok()) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(store_.stream(), &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return;
+  }
+  L.env_seq = pdl_flags_;
+  L.seq = store_.pdl_seq() + 1u;
+}
+
 void Rollout::step() {
   forward_policies(store_.stream(), t_, nullptr, 0, nullptr, false, true);
   if (fused_ok()) {
     TagLaunch L = fused_launch(t_);
-    // Consecutive fused steps overlap through programmatic dependent launch
-    // (per-env waits, TagLaunch::env_seq). With device policies every step
-    // is serialised behind the policy kernels anyway.
-    // Not while the stream is being captured into someone's graph: the
-    // sequence numbers would be baked in and replays would not wait.
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    const bool capturing = cudaStreamIsCapturing(store_.stream(), &cs) != cudaSuccess ||
-                           cs != cudaStreamCaptureStatusNone;
-    if (pol_[0] == nullptr && !capturing && pdl_flags_ != nullptr) {
-      L.env_seq = pdl_flags_;
-      L.seq = store_.pdl_seq() + 1u;
-    }
+    set_pdl(L);
     plan_.launch(L);
     if (L.env_seq != nullptr) store_.commit_pdl_seq();
     ++launches_;
@@ -911,7 +931,8 @@ void Rollout::drop_graph() {
 // *step_dev_ + i, so one instantiated graph replays any window of steps.
 void Rollout::build_graph() {
   drop_graph();
-  if (step_dev_ == nullptr) cuda_check(cudaMalloc(&step_dev_, sizeof(int64_t)), "cudaMalloc(step)");
+  // [0] = first step of the window, [1] = sequence number before it (PDL)
+  if (step_dev_ == nullptr) cuda_check(cudaMalloc(&step_dev_, 2 * sizeof(int64_t)), "cudaMalloc(step)");
   cudaStream_t st = store_.stream();
   cudaStream_t cap = st;
   bool own = false;
@@ -919,6 +940,7 @@ void Rollout::build_graph() {
     cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
     own = true;
   }
+  graph_pdl_ = pol_[0] == nullptr && pdl_flags_ != nullptr && plan_.pdl_ok();
   cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
   cudaError_t err = cudaSuccess;
   for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
@@ -934,6 +956,11 @@ void Rollout::build_graph() {
     L.step_dev = step_dev_;
     L.step_add = i;
     L.action_h0 = h_actions0_;
+    if (graph_pdl_) {  // overlapped nodes (programmatic edges)
+      L.env_seq = pdl_flags_;
+      L.seq_dev = step_dev_ + 1;
+      L.seq_add = static_cast<uint32_t>(i + 1);
+    }
     TagDevConfig d = plan_.dev();
     d.fault_bias = fault_tag_radius_bias();
     err = launch_tag_kernel(d, bind_dev_arrays(store_, plan_.config()), L, cap);
@@ -966,7 +993,9 @@ void Rollout::run(int64_t steps) {
       L.n_steps = k;
       L.step0 = t_;
       L.action_h0 = h_actions0_;
+      set_pdl(L);  // the next window's early envs start in this one's tail
       plan_.launch(L);
+      if (L.env_seq != nullptr) store_.commit_pdl_seq();
       ++launches_;
       t_ += k;
       steps -= k;
@@ -979,9 +1008,14 @@ void Rollout::run(int64_t steps) {
         graph_stream_ != store_.stream()) {
       build_graph();
     }
+    const bool graph_pdl = graph_pdl_;  // as captured
     while (steps >= kGraphSteps) {
-      cuda_check(launch_set_counter(step_dev_, t_, store_.stream()), "set step counter");
+      cuda_check(launch_set_counter(step_dev_, t_, store_.stream(),
+                                    graph_pdl ? static_cast<int64_t>(store_.pdl_seq()) : -1),
+                 "set step counter");
       cuda_check(cudaGraphLaunch(graph_exec_, store_.stream()), "graph launch");
+      if (graph_pdl)
+        for (int i = 0; i < kGraphSteps; ++i) store_.commit_pdl_seq();
       launches_ += 1 + kGraphSteps * (pol_[0] != nullptr ? (pol_[0] == pol_[1] ? 2 : 3) : 1);
       t_ += kGraphSteps;
       steps -= kGraphSteps;

@@ -1269,19 +1269,25 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   // + the barrier order every thread's later loads (generic and, after the
   // proxy fence, the bulk copies) after that step's writes.
   const bool pdl = L.env_seq != nullptr;
+  // graph replays read their base sequence number on device (like the step)
+  const uint32_t seq = L.seq_dev != nullptr ? static_cast<uint32_t>(*L.seq_dev) + L.seq_add : L.seq;
   if (pdl) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
       const int64_t eb = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
       for (int k = 0; k < p.envs_per_cta && eb + k < p.E; ++k) {
         const uint32_t* f = L.env_seq + eb + k;
-        uint32_t v;
+        // relaxed polling (an acquire per poll would invalidate this SM's L1
+        // under the CTAs still working on it), backing off, then one acquire
+        uint32_t v, ns = 32;
         for (;;) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-          if (static_cast<int32_t>(v - (L.seq - 1u)) >= 0) break;
-          __nanosleep(64);
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+          if (static_cast<int32_t>(v - (seq - 1u)) >= 0) break;
+          __nanosleep(ns);
+          ns = ns < 1024 ? 2 * ns : ns;
         }
       }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
@@ -2106,13 +2112,12 @@ obs_done:
   }
   if (n_steps > 1) __syncthreads();  // the next step rewrites the shared state
   }  // multi-step loop
-  if (pdl) {  // publish this CTA's envs to the next launch
-    __threadfence();
+  if (pdl) {  // publish this CTA's envs to the next launch (barrier + one gpu-scope release)
     __syncthreads();
     if (tid == 0) {
       const int64_t eb = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
       for (int k = 0; k < p.envs_per_cta && eb + k < p.E; ++k)
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(L.env_seq + eb + k), "r"(L.seq) : "memory");
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(L.env_seq + eb + k), "r"(seq) : "memory");
     }
   }
 }
@@ -2364,11 +2369,14 @@ cudaError_t launch_restore_zero(const ResetRowDesc* descs, int ndesc, const uint
 }
 
 namespace {
-__global__ void set_counter_kernel(int64_t* ptr, int64_t value) { *ptr = value; }
+__global__ void set_counter_kernel(int64_t* ptr, int64_t value, int64_t value2) {
+  ptr[0] = value;
+  if (value2 >= 0) ptr[1] = value2;
+}
 }  // namespace
 
-cudaError_t launch_set_counter(int64_t* ptr, int64_t value, cudaStream_t st) {
-  set_counter_kernel<<<1, 1, 0, st>>>(ptr, value);
+cudaError_t launch_set_counter(int64_t* ptr, int64_t value, cudaStream_t st, int64_t value2) {
+  set_counter_kernel<<<1, 1, 0, st>>>(ptr, value, value2);
   return cudaGetLastError();
 }
 

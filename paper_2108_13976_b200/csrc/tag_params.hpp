@@ -138,6 +138,8 @@ struct TagLaunch {
   // early envs run in the current step's tail. nullptr = plain launch.
   uint32_t* env_seq = nullptr;
   uint32_t seq = 0;
+  const int64_t* seq_dev = nullptr;  // graph replay: seq = *seq_dev + seq_add
+  uint32_t seq_add = 0;
   // Performance-analysis only (WDG_ABLATE env var, never set by the product,
   // tests or bench): bit0 skip exp/sampling, bit1 skip cell K-NN, bit2 skip
   // obs rows, bit3 skip grid build. Results are WRONG when non-zero.

@@ -542,6 +542,8 @@ def test_off_lattice_state_falls_back_exactly(kw, envs):
 @pytest.mark.parametrize("kw,envs", [
     (dict(num_taggers=200, num_runners=800, obs_mode=O.PARTIAL, episode_length=30, seed=41), 1500),
     (dict(num_taggers=1, num_runners=4, episode_length=9, seed=42), 5000),
+    (dict(num_taggers=40, num_runners=160, obs_mode=O.PARTIAL, episode_length=20, seed=44), 2000),
+    (dict(num_taggers=20, num_runners=80, episode_length=15, seed=45), 1000),
     (dict(variant=O.CONTINUOUS, num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, episode_length=12,
           seed=43), 1200),
 ])
@@ -552,6 +554,7 @@ def test_overlapped_steps_equal_serial_steps(kw, envs, monkeypatch):
     included, several waves of CTAs) must equal the same steps launched one
     after another without overlap (WDG_NO_PDL)."""
     dc, oc = cfg_pair(**kw)
+    monkeypatch.setenv("WDG_PDL", "1")  # overlap even where the plan would not choose it
     ws1 = W.Workspace(dc, envs)
     d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 5)
     monkeypatch.setenv("WDG_NO_PDL", "1")
@@ -560,8 +563,10 @@ def test_overlapped_steps_equal_serial_steps(kw, envs, monkeypatch):
     monkeypatch.delenv("WDG_NO_PDL")
     for _ in range(100):
         d1.step()
+    d1.run(100)  # graph replays / multi-step windows, overlapped
     for _ in range(100):
         d2.step()
+    d2.run(100)
     names = list(O.array_layout(oc, envs).keys())
     d = O.first_divergence(dev_snapshot(ws1, names), dev_snapshot(ws2, names))
     assert d is None, f"overlapped vs serial steps: first divergence {d}"

@@ -15,13 +15,34 @@ SHAPES = {
     "c500": (W.CONTINUOUS, 500, 5, 2000),
     "c2_e1776": (W.DISCRETE, 1000, 5, 1776), "c2_e2368": (W.DISCRETE, 1000, 5, 2368),
     "c2_e1184": (W.DISCRETE, 1000, 5, 1184), "c2_e4000": (W.DISCRETE, 1000, 5, 4000),
+    "d100f": (W.DISCRETE, 100, 0, 2000), "c4": (W.DISCRETE, 5, 0, 2000), "d500f": (W.DISCRETE, 500, 0, 400),
 }
 for name in (sys.argv[1:] or list(SHAPES)):
     var, A, K, E = SHAPES[name]
     T = round(A / 5)
-    cfg = W.TagConfig(variant=var, num_taggers=T, num_runners=A - T, obs_mode=W.PARTIAL, k_nearest=K)
+    if A == 5:
+        T = 1
+    cfg = W.TagConfig(variant=var, num_taggers=T, num_runners=A - T, obs_mode=W.PARTIAL if K else W.FULL,
+                      k_nearest=K or 5)
     os.environ["WDG_NO_MULTISTEP"] = "1"
     sps1, ms1, _ = measure(cfg, E, 200, warmup=5)
     del os.environ["WDG_NO_MULTISTEP"]
     sps2, ms2, _ = measure(cfg, E, 200, warmup=5)
-    print(f"{name}: single {ms1 * 1e3:.1f} us/step ({sps1 / 1e6:.2f}M)  run {ms2 * 1e3:.1f} us/step ({sps2 / 1e6:.2f}M)", flush=True)
+    # RolloutDriver::step loop (the bench's per-step launches)
+    import torch
+    st = torch.cuda.current_stream()
+    ws = W.Workspace(cfg, E, stream=st)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, cfg.seed)
+    for _ in range(5):
+        drv.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(200):
+        drv.step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms3 = e0.elapsed_time(e1) / 200
+    ws.close()
+    print(f"{name}: graph {ms1 * 1e3:.1f} us/step ({sps1 / 1e6:.2f}M)  run {ms2 * 1e3:.1f} us/step "
+          f"({sps2 / 1e6:.2f}M)  step {ms3 * 1e3:.1f} us/step ({E / ms3 / 1e3:.2f}M)", flush=True)
