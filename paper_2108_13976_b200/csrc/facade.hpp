@@ -161,8 +161,9 @@ class TagPlan {
   void launch(TagLaunch L);
   // Whether RolloutDriver::run may use multi-step residency launches.
   bool multistep_ok();
-  // Whether consecutive fused launches overlap (programmatic dependent launch).
-  bool pdl_ok() const;
+  // How consecutive fused launches overlap (programmatic dependent launch):
+  // 0 = not at all, 1 = the next launch is released at CTA entry, 2 = at exit.
+  int pdl_mode() const;
   const wdg_tag_config& config() const { return cfg_; }
   const TagDevConfig& dev() const { return dev_; }
   DataStore& store() { return store_; }

@@ -425,19 +425,21 @@ void TagPlan::launch(TagLaunch L) {
 // K-NN (continuous / non-lattice discrete partial obs) at fewer than 3 waves
 // of CTAs, where it measured 2-18% slower, and grid-path full observations
 // (profiles/sweep_r01.json: single_step vs run_multistep).
-// Overlapping consecutive fused launches (TagLaunch::env_seq) measured, per
-// step at 2000 envs (us, overlapped vs serial): C2 127 vs 135, continuous
-// partial A = 1000 449 vs 476 (A = 300 202 vs 203), grid full obs A = 100 61
-// vs 80, brute partial A = 100 37 vs 44 — but discrete partial grids below 256
-// threads lose (A = 200 / 300 / 500 / 700: 106 / 109 / 103 / 117 vs 86 / 87 /
-// 90 / 112) and so do the tiny packed envs of C4 (10.0 vs 8.2; 22.8 vs 8.6
-// at 10000 envs, 25 envs per CTA), where the per-env waits cost more than the
-// few-microsecond kernels can overlap.
-bool TagPlan::pdl_ok() const {
-  if (const char* env = std::getenv("WDG_PDL")) return std::atoi(env) != 0;  // A/B experiments
-  if (!dev_.use_grid) return dev_.envs_per_cta <= 4 && dev_.threads >= 128;
-  if (!dev_.continuous && dev_.partial) return dev_.threads >= 256;
-  return true;
+// Overlapping consecutive fused launches (TagLaunch::env_seq), measured per
+// step at 2000 envs (us; released at CTA entry / at exit / serial):
+//   C2 127 / 137 / 135; continuous partial A = 1000 449 / - / 476 (A = 300
+//   202 / - / 203); grid full obs A = 100 61 / - / 80; brute partial A = 100
+//   37 / - / 44;
+//   discrete partial grids below 256 threads: A = 300 111 / 85 / 87, A = 500
+//   104 / 88 / 90 (A = 200 / 700 at entry: 106 / 117 vs 86 / 112 serial);
+//   tiny packed envs (C4): 10.1 / 9.5 / 8.2, and 22.8 vs 8.6 at 10000 envs
+//   (25 envs per CTA), where the per-env waits cost more than the
+//   few-microsecond kernels can overlap.
+int TagPlan::pdl_mode() const {
+  if (const char* env = std::getenv("WDG_PDL")) return std::atoi(env);  // A/B experiments
+  if (!dev_.use_grid) return (dev_.envs_per_cta <= 4 && dev_.threads >= 128) ? 1 : 0;
+  if (!dev_.continuous && dev_.partial && dev_.threads < 256) return 2;
+  return 1;
 }
 
 bool TagPlan::multistep_ok() {
@@ -845,7 +847,8 @@ void Rollout::step_unfused() {
 // is being captured into someone's graph: the sequence numbers would be baked
 // in and replays would not wait.
 void Rollout::set_pdl(TagLaunch& L) const {
-  if (pol_[0] != nullptr || pdl_flags_ == nullptr || !plan_.pdl_ok()) return;
+  const int mode = plan_.pdl_mode();
+  if (pol_[0] != nullptr || pdl_flags_ == nullptr || mode == 0) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(store_.stream(), &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
@@ -853,6 +856,7 @@ void Rollout::set_pdl(TagLaunch& L) const {
   }
   L.env_seq = pdl_flags_;
   L.seq = store_.pdl_seq() + 1u;
+  L.pdl_late = mode == 2 ? 1 : 0;
 }
 
 void Rollout::step() {
@@ -940,7 +944,8 @@ void Rollout::build_graph() {
     cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
     own = true;
   }
-  graph_pdl_ = pol_[0] == nullptr && pdl_flags_ != nullptr && plan_.pdl_ok();
+  const int graph_mode = plan_.pdl_mode();
+  graph_pdl_ = pol_[0] == nullptr && pdl_flags_ != nullptr && graph_mode != 0;
   cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
   cudaError_t err = cudaSuccess;
   for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
@@ -960,6 +965,7 @@ void Rollout::build_graph() {
       L.env_seq = pdl_flags_;
       L.seq_dev = step_dev_ + 1;
       L.seq_add = static_cast<uint32_t>(i + 1);
+      L.pdl_late = graph_mode == 2 ? 1 : 0;
     }
     TagDevConfig d = plan_.dev();
     d.fault_bias = fault_tag_radius_bias();

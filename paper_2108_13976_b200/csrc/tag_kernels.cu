@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   // graph replays read their base sequence number on device (like the step)
   const uint32_t seq = L.seq_dev != nullptr ? static_cast<uint32_t>(*L.seq_dev) + L.seq_add : L.seq;
   if (pdl) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!L.pdl_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
       const int64_t eb = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
       for (int k = 0; k < p.envs_per_cta && eb + k < p.E; ++k) {
@@ -2113,6 +2113,7 @@ obs_done:
   if (n_steps > 1) __syncthreads();  // the next step rewrites the shared state
   }  // multi-step loop
   if (pdl) {  // publish this CTA's envs to the next launch (barrier + one gpu-scope release)
+    if (L.pdl_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       const int64_t eb = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;

@@ -547,14 +547,15 @@ def test_off_lattice_state_falls_back_exactly(kw, envs):
     (dict(variant=O.CONTINUOUS, num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, episode_length=12,
           seed=43), 1200),
 ])
-def test_overlapped_steps_equal_serial_steps(kw, envs, monkeypatch):
+@pytest.mark.parametrize("pdl_mode", ["1", "2"])  # next launch released at CTA entry / exit
+def test_overlapped_steps_equal_serial_steps(kw, envs, pdl_mode, monkeypatch):
     """RolloutDriver::step launches consecutive fused steps with programmatic
     dependent launch: a CTA of step t+1 starts once its own envs finished step
     t, inside step t's tail. 100 back-to-back steps (no host sync, resets
     included, several waves of CTAs) must equal the same steps launched one
     after another without overlap (WDG_NO_PDL)."""
     dc, oc = cfg_pair(**kw)
-    monkeypatch.setenv("WDG_PDL", "1")  # overlap even where the plan would not choose it
+    monkeypatch.setenv("WDG_PDL", pdl_mode)  # overlap even where the plan would not choose it
     ws1 = W.Workspace(dc, envs)
     d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 5)
     monkeypatch.setenv("WDG_NO_PDL", "1")
