@@ -186,6 +186,7 @@ struct Bf16Args {
   int32_t step_add;
   uint64_t h0;
   int32_t D, Kp, C, V;  // obs_dim, padded K of layer 1, categories, choices
+  int32_t pdl;          // launched with programmatic dependent launch
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(kBfThreads, WDG_BF16_MIN_BLOCKS) policy_bf16_k
   extern __shared__ __align__(128) uint8_t smb[];
   constexpr int KC1 = KP / 8;  // 16-B chunks per layer-1 row
   const int tid = threadIdx.x, warp = tid >> 5;
+  if (a.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   uint8_t* w1s = smb;
   uint8_t* w2s = w1s + 64 * KP * 2;
   uint8_t* w3s = w2s + 64 * 64 * 2;
@@ -356,6 +358,9 @@ __global__ void __launch_bounds__(kBfThreads, WDG_BF16_MIN_BLOCKS) policy_bf16_k
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  // everything above touched only the weights image; the observations (and
+  // the actions this kernel overwrites) belong to the previous kernels
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   constexpr uint32_t id1 = umma_idesc(128, 64), id3 = umma_idesc(128, 16);
   uint32_t phase = 0;
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(kBfThreads, WDG_BF16_MIN_BLOCKS) policy_bf16_k
     const bool ok = tile < tiles && row_of(tile, e, ag);
     const float* src = a.obs + (e * a.A + ag) * D;
 #pragma unroll
-    for (int k = 0; k < KP; ++k) xr[k] = (ok && k < D) ? __ldg(src + k) : 0.f;
+    for (int k = 0; k < KP; ++k) xr[k] = (ok && k < D) ? src[k] : 0.f;  // coherent: written by the step kernel
   };
   int64_t tile = blockIdx.x;
   fetch(tile);
@@ -674,7 +679,7 @@ bool Policy::bf16_supported() const {
 
 void Policy::forward_sample_bf16(const float* obs, int64_t E, int64_t A, int64_t a0, int64_t a1,
                                  int32_t* actions, double* logits, double* values, const SampleKeys& keys,
-                                 cudaStream_t st, uint32_t* error) const {
+                                 cudaStream_t st, uint32_t* error, bool pdl) const {
   if (obs == nullptr) raise(Errc::invalid_argument, "policy forward: null observations");
   if (a0 < 0 || a1 > A || a0 > a1) raise(Errc::index_out_of_range, "policy forward: bad agent range");
   if (!bf16_supported()) {
@@ -723,6 +728,21 @@ void Policy::forward_sample_bf16(const float* obs, int64_t E, int64_t A, int64_t
   }
   const int64_t tiles = (E * b.n + kBfRows - 1) / kBfRows;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t{sms} * per_sm)));
+  b.pdl = pdl ? 1 : 0;
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kBfThreads);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, kern, static_cast<const uint8_t*>(dimage_), b), "policy bf16 kernel");
+    return;
+  }
   kern<<<grid, kBfThreads, smem, st>>>(dimage_, b);
   cuda_check(cudaGetLastError(), "policy bf16 kernel");
 }

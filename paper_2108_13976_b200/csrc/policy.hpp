@@ -77,7 +77,10 @@ class Policy {
   // [E, A, C] (actions may be nullptr) and optionally f64 logits / values.
   void forward_sample_bf16(const float* obs, int64_t E, int64_t A, int64_t a0, int64_t a1, int32_t* actions,
                            double* logits, double* values, const SampleKeys& keys, cudaStream_t st,
-                           uint32_t* error) const;
+                           uint32_t* error, bool pdl = false) const;
+  // pdl: launch with programmatic dependent launch. The kernel releases the
+  // next launch at entry and runs its prologue (weights to smem, TMEM
+  // allocation) before griddepcontrol.wait, i.e. under the previous kernel's tail.
   // The bf16 tensor-core path covers the reference default dims: hidden
   // {64, 64}, C*V <= 7, obs_dim <= 128.
   bool bf16_supported() const;

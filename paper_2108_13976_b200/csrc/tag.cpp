@@ -779,11 +779,12 @@ void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* ste
     k.step_add = step_add;
     k.h0 = h_actions0_;
     int32_t* act = sample ? static_cast<int32_t*>(store_.device_ptr(store_.handle(kSampledActions))) : nullptr;
+    const bool pdl = pdl_flags_ != nullptr;  // WDG_NO_PDL off switch
     if (pol_[0] == pol_[1]) {
-      pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.A, act, lg, vl, k, st, error_);
+      pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.A, act, lg, vl, k, st, error_, pdl);
     } else {
-      pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.T, act, lg, vl, k, st, error_);
-      pol_[1]->forward_sample_bf16(obs, p.E, p.A, p.T, p.A, act, lg, vl, k, st, error_);
+      pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.T, act, lg, vl, k, st, error_, pdl);
+      pol_[1]->forward_sample_bf16(obs, p.E, p.A, p.T, p.A, act, lg, vl, k, st, error_, pdl);
     }
     return;
   }
@@ -848,6 +849,10 @@ void Rollout::step_unfused() {
 // in and replays would not wait.
 void Rollout::set_pdl(TagLaunch& L) const {
   const int mode = plan_.pdl_mode();
+  if (pol_[0] != nullptr && pdl_flags_ != nullptr && pol_prec_ == kPolicyBF16) {
+    L.pdl_wait = 1;  // behind the bf16 policy kernels: plain PDL (prologue overlap only)
+    return;
+  }
   if (pol_[0] != nullptr || pdl_flags_ == nullptr || mode == 0) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(store_.stream(), &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {

@@ -1268,6 +1268,10 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   // launch now, then wait for this CTA's envs' previous step only. ld.acquire
   // + the barrier order every thread's later loads (generic and, after the
   // proxy fence, the bulk copies) after that step's writes.
+  if (L.pdl_wait) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const bool pdl = L.env_seq != nullptr;
   // graph replays read their base sequence number on device (like the step)
   const uint32_t seq = L.seq_dev != nullptr ? static_cast<uint32_t>(*L.seq_dev) + L.seq_add : L.seq;
@@ -2281,7 +2285,7 @@ cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const T
                                            p.smem_bytes);
     if (err != cudaSuccess) return err;
   }
-  if (L.env_seq != nullptr) {
+  if (L.env_seq != nullptr || L.pdl_wait) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(p.grid_ctas));
     cfg.blockDim = dim3(static_cast<unsigned>(p.threads));

@@ -141,6 +141,9 @@ struct TagLaunch {
   const int64_t* seq_dev = nullptr;  // graph replay: seq = *seq_dev + seq_add
   uint32_t seq_add = 0;
   int32_t pdl_late = 0;              // trigger the next launch at exit instead of entry
+  // Plain PDL behind device policy kernels: release the next launch at entry,
+  // then griddepcontrol.wait for the previous kernels (no per-env flags).
+  int32_t pdl_wait = 0;
   // Performance-analysis only (WDG_ABLATE env var, never set by the product,
   // tests or bench): bit0 skip exp/sampling, bit1 skip cell K-NN, bit2 skip
   // obs rows, bit3 skip grid build. Results are WRONG when non-zero.
