@@ -1044,6 +1044,10 @@ void Rollout::check() {
     cudaMemsetAsync(error_, 0, sizeof(uint32_t), store_.stream());
     raise(Errc::non_finite, "sample_actions: non-finite logit (fused rollout)");
   }
+  if (err & kErrStepOrder) {
+    cudaMemsetAsync(error_, 0, sizeof(uint32_t), store_.stream());
+    raise(Errc::cuda, "fused rollout: an overlapped step timed out waiting for the previous step");
+  }
 }
 
 void Rollout::stats(double* out, int32_t count) {

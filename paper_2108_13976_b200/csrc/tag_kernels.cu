@@ -1283,10 +1283,14 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         const uint32_t* f = L.env_seq + eb + k;
         // relaxed polling (an acquire per poll would invalidate this SM's L1
         // under the CTAs still working on it), backing off, then one acquire
-        uint32_t v, ns = 32;
+        uint32_t v, ns = 32, polls = 0;
         for (;;) {
           asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
           if (static_cast<int32_t>(v - (seq - 1u)) >= 0) break;
+          if (++polls > (1u << 22)) {  // >= 4 s of polling: report, never hang the device
+            if (L.error) atomicOr(L.error, kErrStepOrder);
+            break;
+          }
           __nanosleep(ns);
           ns = ns < 1024 ? 2 * ns : ns;
         }

@@ -31,7 +31,9 @@ enum TagMode : int32_t {
 };
 
 // Sticky device error bits (read at sync points, mapped to wdg_status).
-enum : uint32_t { kErrNonFinite = 1u, kErrBadAction = 2u };
+// kErrStepOrder: an overlapped launch gave up waiting (seconds) for its envs'
+// previous step (TagLaunch::env_seq) instead of hanging the device.
+enum : uint32_t { kErrNonFinite = 1u, kErrBadAction = 2u, kErrStepOrder = 4u };
 
 // Raw device addresses of one store's Tag arrays (tag_env.cpp:47-79 `Arrays`).
 struct TagDevArrays {
