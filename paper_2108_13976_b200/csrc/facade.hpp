@@ -162,7 +162,8 @@ class TagPlan {
   // Whether RolloutDriver::run may use multi-step residency launches.
   bool multistep_ok();
   // How consecutive fused launches overlap (programmatic dependent launch):
-  // 0 = not at all, 1 = the next launch is released at CTA entry, 2 = at exit.
+  // 0 = not at all, 1 = the next launch is released at CTA entry, 2 = at exit
+  // (both with per-env waits), 3 = plain PDL (released at entry, whole-grid wait).
   int pdl_mode() const;
   const wdg_tag_config& config() const { return cfg_; }
   const TagDevConfig& dev() const { return dev_; }
@@ -278,7 +279,7 @@ class Rollout {
   uint64_t h_actions0_ = 0;
   uint32_t* pdl_flags_ = nullptr;  // the store's (DataStore::pdl_flags)
   bool graph_pdl_ = false;         // the captured graph's nodes overlap (PDL)
-  void set_pdl(TagLaunch& L) const;
+  void set_pdl(TagLaunch& L, bool single_step) const;
   // host-driven stepping: double-buffered logits + copy stream
   cudaStream_t copy_ = nullptr;
   double* dlog_[2] = {nullptr, nullptr};

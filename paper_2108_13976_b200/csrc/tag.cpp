@@ -433,11 +433,12 @@ void TagPlan::launch(TagLaunch L) {
 //   discrete partial grids below 256 threads: A = 300 111 / 85 / 87, A = 500
 //   104 / 88 / 90 (A = 200 / 700 at entry: 106 / 117 vs 86 / 112 serial);
 //   tiny packed envs (C4): 10.1 / 9.5 / 8.2, and 22.8 vs 8.6 at 10000 envs
-//   (25 envs per CTA), where the per-env waits cost more than the
-//   few-microsecond kernels can overlap.
+//   (25 envs per CTA): the per-env waits cost more than the few-microsecond
+//   kernels can overlap. Plain PDL (release at entry, whole-grid
+//   griddepcontrol.wait) still hides the launch gap there: 6.9 vs 8.2.
 int TagPlan::pdl_mode() const {
   if (const char* env = std::getenv("WDG_PDL")) return std::atoi(env);  // A/B experiments
-  if (!dev_.use_grid) return (dev_.envs_per_cta <= 4 && dev_.threads >= 128) ? 1 : 0;
+  if (!dev_.use_grid) return (dev_.envs_per_cta <= 4 && dev_.threads >= 128) ? 1 : 3;
   if (!dev_.continuous && dev_.partial && dev_.threads < 256) return 2;
   return 1;
 }
@@ -847,13 +848,17 @@ void Rollout::step_unfused() {
 // is serialised behind the policy kernels anyway), and not while the stream
 // is being captured into someone's graph: the sequence numbers would be baked
 // in and replays would not wait.
-void Rollout::set_pdl(TagLaunch& L) const {
+void Rollout::set_pdl(TagLaunch& L, bool single_step) const {
   const int mode = plan_.pdl_mode();
   if (pol_[0] != nullptr && pdl_flags_ != nullptr && pol_prec_ == kPolicyBF16) {
     L.pdl_wait = 1;  // behind the bf16 policy kernels: plain PDL (prologue overlap only)
     return;
   }
   if (pol_[0] != nullptr || pdl_flags_ == nullptr || mode == 0) return;
+  if (mode == 3) {  // plain PDL: next launch released at entry, griddepcontrol.wait, no flags
+    L.pdl_wait = single_step ? 1 : 0;  // neutral to worse for multi-step windows and graphs
+    return;
+  }
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(store_.stream(), &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
@@ -868,7 +873,7 @@ void Rollout::step() {
   forward_policies(store_.stream(), t_, nullptr, 0, nullptr, false, true);
   if (fused_ok()) {
     TagLaunch L = fused_launch(t_);
-    set_pdl(L);
+    set_pdl(L, true);
     plan_.launch(L);
     if (L.env_seq != nullptr) store_.commit_pdl_seq();
     ++launches_;
@@ -950,7 +955,7 @@ void Rollout::build_graph() {
     own = true;
   }
   const int graph_mode = plan_.pdl_mode();
-  graph_pdl_ = pol_[0] == nullptr && pdl_flags_ != nullptr && graph_mode != 0;
+  graph_pdl_ = pol_[0] == nullptr && pdl_flags_ != nullptr && graph_mode != 0 && graph_mode != 3;
   cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
   cudaError_t err = cudaSuccess;
   for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
@@ -1004,7 +1009,7 @@ void Rollout::run(int64_t steps) {
       L.n_steps = k;
       L.step0 = t_;
       L.action_h0 = h_actions0_;
-      set_pdl(L);  // the next window's early envs start in this one's tail
+      set_pdl(L, false);  // the next window's early envs start in this one's tail
       plan_.launch(L);
       if (L.env_seq != nullptr) store_.commit_pdl_seq();
       ++launches_;
@@ -1019,7 +1024,7 @@ void Rollout::run(int64_t steps) {
         graph_stream_ != store_.stream()) {
       build_graph();
     }
-    const bool graph_pdl = graph_pdl_;  // as captured
+    const bool graph_pdl = graph_pdl_;  // as captured (flag sequence numbers)
     while (steps >= kGraphSteps) {
       cuda_check(launch_set_counter(step_dev_, t_, store_.stream(),
                                     graph_pdl ? static_cast<int64_t>(store_.pdl_seq()) : -1),

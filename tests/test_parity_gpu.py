@@ -547,7 +547,7 @@ def test_off_lattice_state_falls_back_exactly(kw, envs):
     (dict(variant=O.CONTINUOUS, num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, episode_length=12,
           seed=43), 1200),
 ])
-@pytest.mark.parametrize("pdl_mode", ["1", "2"])  # next launch released at CTA entry / exit
+@pytest.mark.parametrize("pdl_mode", ["1", "2", "3"])  # per-env waits, released at entry / exit; plain PDL
 def test_overlapped_steps_equal_serial_steps(kw, envs, pdl_mode, monkeypatch):
     """RolloutDriver::step launches consecutive fused steps with programmatic
     dependent launch: a CTA of step t+1 starts once its own envs finished step
