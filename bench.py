@@ -362,6 +362,9 @@ def run_ours(args, rank, world, local_rank):
                          "kernel": "tag_env_kernel<discrete,partial,grid> (fused step)"},
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": n_logits * 8, "d2h_bytes_per_step": E * A * 4 + E,
+                    # per-rank PCIe upload rate implied by the e2e value (bound: the link's
+                    # pinned H2D rate, 55.3 GB/s measured by tools/h2d_probe.py)
+                    "h2d_gbs": (e2e_value / world) / E * n_logits * 8 / 1e9,
                     "path": "wdg_rollout_step_host (pinned host logits -> fused kernel -> rewards+done)"},
             "sampler_stress": {"logits": "N(0, 3^2), seed 1234", "steps": stress_steps,
                                "env_steps_per_s": E * stress_steps / (stress_ms / 1e3),
