@@ -371,6 +371,7 @@ def run_ours(args, rank, world, local_rank):
                                "ms_per_step": stress_ms / stress_steps},
             "policy_rollout": policy_leg,
             "run_multistep": multistep_leg,
+            "per_gpu_value": value / world,  # aggregate and per-GPU env-steps/s
             "gpu_launches": launches,
             "episode_stats": {"episodes": stats[0], "tag_events": stats[3], "env_steps": stats[4]},
             "clocks": clocks.summary(),
