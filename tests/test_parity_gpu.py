@@ -574,3 +574,22 @@ def test_overlapped_steps_equal_serial_steps(kw, envs, pdl_mode, monkeypatch):
     np.testing.assert_array_equal(d1.stats(), d2.stats())
     ws1.close()
     ws2.close()
+
+
+def test_spec_tag_examples_device():
+    """SPEC.md:245-267 known answers (lowest-index credit among same-cell
+    taggers, +2 for two simultaneous credits, -1 for a tagged runner, zero
+    observations once inactive) on the device step, and equal to the oracle."""
+    from test_oracle_pinning import check_spec_tag_scene, spec_tag_scene
+    oc, x, y = spec_tag_scene()
+    dc = W.TagConfig(**{f: getattr(oc, f) for f, _ in O.TagConfigC._fields_})
+    ws = W.Workspace(dc, 1)
+    o = O.OracleWorld(oc, 1)
+    for name, arr in (("loc_x", x), ("loc_y", y), ("sampled_actions", np.zeros((1, 5, 1), np.int32))):
+        ws.store.push(name, arr)
+        o.push(name, arr)
+    ws.engine.run_step(ws.plan, ws.store, 0)
+    o.step(0)
+    check_spec_tag_scene(ws.store.pull)
+    assert_same(dev_snapshot(ws, o.layout), o.snapshot(), "SPEC tag scene")
+    ws.close()
