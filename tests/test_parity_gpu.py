@@ -593,3 +593,21 @@ def test_spec_tag_examples_device():
     check_spec_tag_scene(ws.store.pull)
     assert_same(dev_snapshot(ws, o.layout), o.snapshot(), "SPEC tag scene")
     ws.close()
+
+
+def test_spec_continuous_tie_device():
+    """Continuous equidistant taggers: the lower index is credited (min over
+    (d^2, index)), on the device step, equal to the oracle."""
+    from test_oracle_pinning import check_spec_continuous_tie, spec_continuous_tie_scene
+    oc, state = spec_continuous_tie_scene()
+    dc = W.TagConfig(**{f: getattr(oc, f) for f, _ in O.TagConfigC._fields_})
+    ws = W.Workspace(dc, 1)
+    o = O.OracleWorld(oc, 1)
+    for n, v in state.items():
+        ws.store.push(n, v)
+        o.push(n, v)
+    ws.engine.run_step(ws.plan, ws.store, 0)
+    o.step(0)
+    check_spec_continuous_tie(ws.store.pull)
+    assert_same(dev_snapshot(ws, o.layout), o.snapshot(), "continuous tie scene", cont=True)
+    ws.close()
