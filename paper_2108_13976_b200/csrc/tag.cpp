@@ -275,7 +275,7 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     p.off_cfill = take(4 * (p.ncells + 1), 4);
     p.off_items = take(2 * A, 4);
     p.off_cellof = take(2 * A, 4);
-    if (p.lattice && p.partial && p.stage_obs) p.off_cellknn = take(2 * int64_t{p.ncells} * (p.K + 1), 4);
+    if (p.lattice && p.partial) p.off_cellknn = take(2 * int64_t{p.ncells} * (p.K + 1), 4);
     p.off_cellact = take(p.ncells, 16);
   }
   p.env_bytes = align16(off);

@@ -1754,7 +1754,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           s.cs[a] = cos_ref(s.dir[a]);
         }
       }
-      if (PARTIAL && !CONT && GRID && p.lattice && all_integral && p.stage_obs)
+      if (PARTIAL && !CONT && GRID && p.lattice && all_integral)
         build_cell_lists(s, p, L.ablate);
     }
     __syncthreads();
@@ -2038,9 +2038,30 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   } else if constexpr (!(EXACT && PARTIAL)) {
     // Wide rows (full obs, large A): K-NN into smem, then the CTA writes its
     // contiguous [envs, A, D] block cooperatively (coalesced).
+    // Lattice envs copy each agent's K nearest from its cell's (K+1)-list
+    // (self dropped) instead of a per-agent top-K, whose MAXK = 32 register
+    // list spills at large K (K = 20 at C2: 26.8 ms -> see DESIGN).
+    const bool cell_lists = PARTIAL && lattice_ok;  // GRID => single env per CTA
+    const int kk = p.K + 1;
+    if (cell_lists && !early_inputs) {
+      build_cell_lists(s, p, L.ablate);
+      __syncthreads();
+    }
     if (PARTIAL && live) {
       for (int a = lt; a < A; a += tpe) {
         if (!s.act[a]) continue;
+        if (cell_lists) {
+          const int cl = s.cellof[a];
+          if (s.cfill[cl] == kk) {
+            const uint16_t* lst = s.cellknn + cl * kk;
+            int w = 0;
+            for (int t = 0; t < kk; ++t) {
+              const int j = lst[t];
+              if (j != a && w < p.K) s.knn[a * p.K + w++] = static_cast<uint16_t>(j);
+            }
+            continue;
+          }
+        }
         TopK<MAXK, EXACT> top;
         knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top, brute_keys, disc_integral);
 #pragma unroll

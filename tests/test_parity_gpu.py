@@ -77,6 +77,9 @@ CONFIGS = {
     # brute-force K-NN at 150 agents (grid less than half occupied)
     "disc_part_4x150": (dict(num_taggers=30, num_runners=120, obs_mode=O.PARTIAL, episode_length=50,
                              seed=11), 4),
+    # K=20 (obs rows of 83 floats, the cooperative wide-row writer) on lattice cells
+    "disc_part_2x300_k20": (dict(num_taggers=60, num_runners=240, obs_mode=O.PARTIAL, k_nearest=20,
+                                 episode_length=25, seed=14), 2),
     # 3000 agents on a 40 x 40 lattice (12 agent strides per thread, 1600 cells)
     "disc_part_2x3000_g40": (dict(num_taggers=600, num_runners=2400, obs_mode=O.PARTIAL, grid_size=40,
                                   episode_length=20, seed=13), 2),
