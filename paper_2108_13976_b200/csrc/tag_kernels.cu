@@ -1182,11 +1182,13 @@ constexpr int kSlotT = 16, kSlotR = 48;
 // Discrete full-observation rows of a one-env CTA (write_obs_row,
 // tag_env.cpp:165-212, every other agent in ascending order): one warp per
 // row, lane l always writes component l & 3 of neighbour block f >> 2.
+// (partial = true: the neighbours are the agent's K nearest in s.knn, the
+// wide partial rows of K >= 16)
 __device__ __forceinline__ void write_full_rows_discrete(const EnvSmem& s, const TagDevConfig& p, float* cta_out,
-                                                     int A, int D, int32_t step_count) {
+                                                     int A, int D, int32_t step_count, bool partial = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-  const int nb_f = 4 * (A - 1);
+  const int nb_f = 4 * (partial ? p.K : A - 1);
   const int comp = lane & 3;
   const float iw = p.inv_world;
   const float* fsrc = comp == 0 ? s.x : s.y;
@@ -1200,7 +1202,7 @@ __device__ __forceinline__ void write_full_rows_discrete(const EnvSmem& s, const
     const float so = comp == 0 ? s.x[a] : s.y[a];
     for (int f = lane; f < nb_f; f += 32) {
       const int nn = f >> 2;
-      const int j = nn + (nn >= a ? 1 : 0);
+      const int j = partial ? static_cast<int>(s.knn[a * p.K + nn]) : nn + (nn >= a ? 1 : 0);
       float v;
       if (comp < 2) {
         v = __fmul_rn(__fsub_rn(fsrc[j], so), iw);
@@ -2078,6 +2080,12 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         // same component (l & 3) of neighbour block f >> 2 — branch-light,
         // 128-byte coalesced streaming stores.
         write_full_rows_discrete(s, p, cta_out, A, D, sc.step_count);
+        goto obs_done;
+      }
+    }
+    if constexpr (PARTIAL && !CONT) {
+      if (single) {  // wide partial rows (K >= 16): the same warp-per-row writer
+        write_full_rows_discrete(s, p, cta_out, A, D, sc.step_count, true);
         goto obs_done;
       }
     }
