@@ -77,6 +77,12 @@ CONFIGS = {
     # brute-force K-NN at 150 agents (grid less than half occupied)
     "disc_part_4x150": (dict(num_taggers=30, num_runners=120, obs_mode=O.PARTIAL, episode_length=50,
                              seed=11), 4),
+    # K=8 at 400 agents on lattice cells (generic MAXK=8 instantiation)
+    "disc_part_2x400_k8": (dict(num_taggers=80, num_runners=320, obs_mode=O.PARTIAL, k_nearest=8,
+                                episode_length=25, seed=15), 2),
+    # K=1 on lattice cells (compile-time K=1)
+    "disc_part_2x400_k1": (dict(num_taggers=80, num_runners=320, obs_mode=O.PARTIAL, k_nearest=1,
+                                episode_length=25, seed=16), 2),
     # K=20 (obs rows of 83 floats, the cooperative wide-row writer) on lattice cells
     "disc_part_2x300_k20": (dict(num_taggers=60, num_runners=240, obs_mode=O.PARTIAL, k_nearest=20,
                                  episode_length=25, seed=14), 2),

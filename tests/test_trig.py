@@ -52,6 +52,9 @@ CONT = {
     # runtime K (non-exact instantiations): K=3 brute-force, K=12 ring search (MAXK 32)
     "cont_part_9x30_k3": (dict(variant=O.CONTINUOUS, num_taggers=6, num_runners=24, obs_mode=O.PARTIAL,
                                k_nearest=3, episode_length=35, world_length=6.0, seed=8), 9),
+    "cont_part_2x300_k8": (dict(variant=O.CONTINUOUS, num_taggers=60, num_runners=240, obs_mode=O.PARTIAL,
+                                k_nearest=8, episode_length=30, world_length=14.0, tag_radius=0.6,
+                                seed=10), 2),
     "cont_part_2x400_k12": (dict(variant=O.CONTINUOUS, num_taggers=80, num_runners=320, obs_mode=O.PARTIAL,
                                  k_nearest=12, episode_length=30, world_length=16.0, tag_radius=0.6,
                                  seed=9), 2),
