@@ -522,6 +522,7 @@ def test_graph_replay_equals_direct_launches(kw, envs):
     (dict(num_taggers=20, num_runners=80, obs_mode=O.PARTIAL, seed=32), 4),   # one-env brute
     (dict(num_taggers=40, num_runners=160, obs_mode=O.PARTIAL, seed=33), 3),  # lattice cells
     (dict(num_taggers=20, num_runners=80, seed=34), 4),                        # full obs, grid resolve
+    (dict(num_taggers=60, num_runners=240, obs_mode=O.PARTIAL, k_nearest=20, seed=35), 2),  # wide rows
 ])
 def test_off_lattice_state_falls_back_exactly(kw, envs):
     """Pushed state outside what placement produces — half-integer positions
