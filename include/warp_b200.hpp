@@ -301,9 +301,13 @@ class RolloutDriver {
                                    static_cast<int32_t>(prec)));
   }
   void step() { check(wdg_rollout_step(h_)); }
-  void step_host(const double* host_logits, int64_t count, float* host_rewards, uint8_t* host_done) {
-    check(wdg_rollout_step_host(h_, host_logits, count, host_rewards, host_done));
+  // Host-buffer step: rewards / done before reset-on-done, observations
+  // after it (pass host_obs = nullptr to skip them).
+  void step_host(const double* host_logits, int64_t count, float* host_rewards, uint8_t* host_done,
+                 float* host_obs = nullptr, int64_t obs_count = 0) {
+    check(wdg_rollout_step_host_obs(h_, host_logits, count, host_rewards, host_done, host_obs, obs_count));
   }
+  void set_host_chunks(int32_t chunks) { check(wdg_rollout_set_host_chunks(h_, chunks)); }
   void run(int64_t steps) { check(wdg_rollout_run(h_, steps)); }
   void check_errors() { check(wdg_rollout_check(h_)); }
   std::vector<double> stats() {

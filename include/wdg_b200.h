@@ -239,18 +239,44 @@ WDG_API void wdg_rollout_destroy(wdg_rollout* rollout);
 WDG_API wdg_status wdg_rollout_set_logits(wdg_rollout* rollout, const double* logits,
                                           int64_t logits_count);
 WDG_API wdg_status wdg_rollout_set_fused(wdg_rollout* rollout, int32_t fused);
+/* Overlap consecutive fused launches (programmatic dependent launch with
+ * per-env sequence flags, default on); 0 = each launch waits for the previous
+ * one to finish. Results are identical either way. */
+WDG_API wdg_status wdg_rollout_set_overlap(wdg_rollout* rollout, int32_t enabled);
+/* Plan tuning overrides for A/B measurements and path-pinning tests: how a
+ * plan maps the step onto the GPU, never what it computes. Keys:
+ * stage_rows, brute_max, threads_per_env_max, cont_cell_div, disc_grid_cells,
+ * stage_obs, bulk_in, l2_prefetch, pdl_mode, multistep; value < 0 restores
+ * the plan's own choice; key "reset" restores all. Read when a plan is built
+ * (geometry) or a rollout launches (pdl_mode, multistep). */
+WDG_API wdg_status wdg_set_tuning(const char* key, int64_t value);
 /* Use CUDA-graph replay for wdg_rollout_run (default on). */
 WDG_API wdg_status wdg_rollout_set_graphs(wdg_rollout* rollout, int32_t enabled);
 WDG_API wdg_status wdg_rollout_step(wdg_rollout* rollout);
-/* One step driven from HOST buffers (the drop-in host integration): the
- * step's f64 logits [E,A,C,V] are copied host->device (double-buffered on a
- * copy stream so the copy of step t+1 overlaps the kernel of step t), the
- * fused step runs, and the step's rewards [E,A] f32 and done [E] u8 are copied
- * device->host. Asynchronous: results are valid after wdg_store_synchronize.
- * Host buffers should be pinned; host_rewards / host_done may be NULL. */
+/* One step driven from HOST buffers (the drop-in host integration; replaces
+ * the reference learner's host loop sample_actions(host logits) -> run_step ->
+ * post_step reads -> auto_reset, trainer.cpp:357-397 / harness.cpp:478-490):
+ * the step's f64 logits [E,A,C,V] go host->device, the fused step runs, and
+ * the step's rewards [E,A] f32 and done [E] u8 come back device->host as they
+ * were BEFORE reset-on-done (the post_step hook's view, trainer.cpp:382-394),
+ * so a finished env reports done = 1 and its terminal rewards. The step is
+ * pipelined over env chunks (H2D, kernel and D2H of different chunks overlap).
+ * Asynchronous: the host buffers are read / written until
+ * wdg_store_synchronize returns. Host buffers should be pinned;
+ * host_rewards / host_done may be NULL. */
 WDG_API wdg_status wdg_rollout_step_host(wdg_rollout* rollout, const double* host_logits,
                                          int64_t logits_count, float* host_rewards,
                                          uint8_t* host_done);
+/* The same step, also returning the observations [E,A,D] f32 AFTER the step
+ * and its reset-on-done: what the next policy_forward reads
+ * (trainer.cpp:358-360). host_obs may be NULL (obs_count is then ignored). */
+WDG_API wdg_status wdg_rollout_step_host_obs(wdg_rollout* rollout, const double* host_logits,
+                                             int64_t logits_count, float* host_rewards,
+                                             uint8_t* host_done, float* host_obs,
+                                             int64_t obs_count);
+/* Env chunks of the pipelined host step (0 = automatic: ~8 MB of logits per
+ * chunk, at most 16). */
+WDG_API wdg_status wdg_rollout_set_host_chunks(wdg_rollout* rollout, int32_t chunks);
 WDG_API wdg_status wdg_rollout_run(wdg_rollout* rollout, int64_t steps);
 WDG_API wdg_status wdg_rollout_next_step(const wdg_rollout* rollout, int64_t* out);
 /* Kernel launches issued so far (step kernels, policy forwards, graph nodes). */

@@ -69,7 +69,9 @@ EXPORTED_SYMBOLS = [
     "wdg_episodes_started", "wdg_rollout_create", "wdg_rollout_destroy", "wdg_rollout_set_logits",
     "wdg_rollout_set_fused", "wdg_rollout_set_graphs", "wdg_rollout_step", "wdg_rollout_run",
     "wdg_rollout_next_step", "wdg_rollout_check", "wdg_rollout_stats", "wdg_rollout_reset_stats",
-    "wdg_rollout_stats_device_ptr", "wdg_rollout_step_host", "wdg_rollout_reduce_stats_into",
+    "wdg_rollout_stats_device_ptr", "wdg_rollout_step_host", "wdg_rollout_step_host_obs",
+    "wdg_rollout_set_host_chunks", "wdg_rollout_reduce_stats_into", "wdg_rollout_set_overlap",
+    "wdg_set_tuning",
     "wdg_policy_create", "wdg_policy_destroy", "wdg_policy_init", "wdg_policy_param_count",
     "wdg_policy_set_params", "wdg_policy_get_params", "wdg_policy_forward", "wdg_rollout_set_policies",
     "wdg_rollout_policy_outputs", "wdg_copy_to_host", "wdg_rollout_set_keep_policy_outputs",
@@ -188,6 +190,10 @@ def _load():
         "wdg_rollout_reset_stats": (I32, [P]),
         "wdg_rollout_stats_device_ptr": (I32, [P, C.POINTER(C.POINTER(D))]),
         "wdg_rollout_step_host": (I32, [P, P, I64, P, P]),
+        "wdg_rollout_step_host_obs": (I32, [P, P, I64, P, P, P, I64]),
+        "wdg_rollout_set_host_chunks": (I32, [P, I32]),
+        "wdg_rollout_set_overlap": (I32, [P, I32]),
+        "wdg_set_tuning": (I32, [C.c_char_p, I64]),
         "wdg_rollout_reduce_stats_into": (I32, [P, P]),
         "wdg_policy_create": (I32, [I64, C.POINTER(I64), I32, I64, I64, C.POINTER(P)]),
         "wdg_policy_destroy": (None, [P]),
@@ -265,6 +271,13 @@ def set_fault_tag_radius_bias(bias: float):
     """detail::fault_hooks().tag_radius_bias (tag_env.hpp:155-158): test-only
     mutation of the device kernels' tag radius."""
     _load().wdg_set_fault_tag_radius_bias(float(bias))
+
+
+def set_tuning(key: str, value: int = -1):
+    """Plan tuning override (wdg_set_tuning): how a plan maps the step onto
+    the GPU, never what it computes; value < 0 or key "reset" restores the
+    plan's own choice."""
+    _check(_load().wdg_set_tuning(key.encode(), value))
 
 
 def _ptr(x) -> int:
@@ -650,20 +663,38 @@ class RolloutDriver:
     def set_graphs(self, enabled: bool):
         _check(self._lib.wdg_rollout_set_graphs(self._h, 1 if enabled else 0))
 
+    def set_overlap(self, enabled: bool):
+        """Overlapped consecutive launches (default on); off = serial launches."""
+        _check(self._lib.wdg_rollout_set_overlap(self._h, 1 if enabled else 0))
+
     def step(self):
         _check(self._lib.wdg_rollout_step(self._h))
 
-    def step_host(self, host_logits, count: int, host_rewards=None, host_done=None):
+    def step_host(self, host_logits, count: int, host_rewards=None, host_done=None,
+                  host_obs=None, obs_count: int = 0):
         """One step from HOST buffers (addresses or pinned CPU tensors /
-        numpy arrays); results valid after store.synchronize()."""
+        numpy arrays): rewards and done as they were before reset-on-done
+        (trainer.cpp:382-394), observations after it; results valid after
+        store.synchronize()."""
         def hp(x):
             if x is None:
                 return None
             if isinstance(x, np.ndarray):
                 return x.ctypes.data
             return _ptr(x)
-        _check(self._lib.wdg_rollout_step_host(self._h, C.c_void_p(hp(host_logits)), count,
-                                               C.c_void_p(hp(host_rewards)), C.c_void_p(hp(host_done))))
+        if host_obs is None:
+            _check(self._lib.wdg_rollout_step_host(self._h, C.c_void_p(hp(host_logits)), count,
+                                                   C.c_void_p(hp(host_rewards)),
+                                                   C.c_void_p(hp(host_done))))
+        else:
+            _check(self._lib.wdg_rollout_step_host_obs(self._h, C.c_void_p(hp(host_logits)), count,
+                                                       C.c_void_p(hp(host_rewards)),
+                                                       C.c_void_p(hp(host_done)),
+                                                       C.c_void_p(hp(host_obs)), obs_count))
+
+    def set_host_chunks(self, chunks: int):
+        """Env chunks of the pipelined step_host (0 = automatic)."""
+        _check(self._lib.wdg_rollout_set_host_chunks(self._h, chunks))
 
     def reduce_stats_into(self, device_out):
         _check(self._lib.wdg_rollout_reduce_stats_into(self._h, C.c_void_p(_ptr(device_out))))

@@ -375,6 +375,17 @@ wdg_status wdg_rollout_set_fused(wdg_rollout* r, int32_t fused) {
   return guarded([&] { need(r, "rollout")->impl->set_fused(fused != 0); });
 }
 
+wdg_status wdg_rollout_set_overlap(wdg_rollout* r, int32_t enabled) {
+  return guarded([&] { need(r, "rollout")->impl->set_overlap(enabled != 0); });
+}
+
+wdg_status wdg_set_tuning(const char* key, int64_t value) {
+  return guarded([&] {
+    if (key == nullptr) wdg::raise(wdg::Errc::invalid_argument, "set_tuning: null key");
+    wdg::set_tuning(key, value);
+  });
+}
+
 wdg_status wdg_rollout_set_graphs(wdg_rollout* r, int32_t enabled) {
   return guarded([&] { need(r, "rollout")->impl->set_graphs(enabled != 0); });
 }
@@ -387,6 +398,21 @@ wdg_status wdg_rollout_step_host(wdg_rollout* r, const double* host_logits, int6
                                  float* host_rewards, uint8_t* host_done) {
   return guarded([&] {
     need(r, "rollout")->impl->step_host(host_logits, count, host_rewards, host_done);
+  });
+}
+
+wdg_status wdg_rollout_step_host_obs(wdg_rollout* r, const double* host_logits, int64_t count,
+                                     float* host_rewards, uint8_t* host_done, float* host_obs,
+                                     int64_t obs_count) {
+  return guarded([&] {
+    need(r, "rollout")->impl->step_host(host_logits, count, host_rewards, host_done, host_obs, obs_count);
+  });
+}
+
+wdg_status wdg_rollout_set_host_chunks(wdg_rollout* r, int32_t chunks) {
+  return guarded([&] {
+    if (chunks < 0) wdg::raise(wdg::Errc::invalid_argument, "set_host_chunks: chunks must be >= 0");
+    need(r, "rollout")->impl->set_host_chunks(chunks);
   });
 }
 

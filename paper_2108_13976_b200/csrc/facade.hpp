@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -114,6 +115,16 @@ class DataStore {
   uint32_t* pdl_flags();
   uint32_t pdl_seq() const noexcept { return pdl_seq_; }
   void commit_pdl_seq() noexcept { ++pdl_seq_; }
+  // Resynchronise the flags after a skipped (timed-out) overlapped step.
+  void reset_pdl();
+  // True when the last kernel a rollout enqueued on this store's stream
+  // released its dependents early (griddepcontrol.launch_dependents: bf16
+  // policy forwards, plain-PDL Tag launches) WITHOUT publishing env_seq
+  // flags. A flag-waiting launch after it must also griddepcontrol.wait:
+  // its flag test is already satisfied by older launches, so it would
+  // otherwise start while that kernel still writes the envs.
+  bool pdl_open() const noexcept { return pdl_open_; }
+  void set_pdl_open(bool open) noexcept { pdl_open_ = open; }
 
  private:
   struct Entry {
@@ -139,6 +150,7 @@ class DataStore {
   int32_t descs_cap_ = 0;
   uint32_t* pdl_flags_ = nullptr;
   uint32_t pdl_seq_ = 0;
+  bool pdl_open_ = false;
   friend class ResetManager;
 };
 
@@ -159,6 +171,8 @@ class TagPlan {
   void run_step(int64_t step_index);
   void reinit_masked(const uint8_t* env_mask, int32_t* episode);
   void launch(TagLaunch L);
+  // The same launch restricted to envs [e0, e0 + n) (pipelined host steps).
+  void launch_envs(TagLaunch L, int64_t e0, int64_t n);
   // Whether RolloutDriver::run may use multi-step residency launches.
   bool multistep_ok();
   // How consecutive fused launches overlap (programmatic dependent launch):
@@ -234,10 +248,16 @@ class Rollout {
   const double* policy_values() const { return pol_values_; }
   void set_fused(bool f) { fused_ = f; }
   void set_graphs(bool g) { graphs_ = g; }
+  // Overlap consecutive launches (programmatic dependent launch, default on);
+  // off = one plain launch after another (A/B timing, serial references).
+  void set_overlap(bool enabled);
   void step();
   // Trainer::collect (trainer.cpp:315-403): T captured policy steps.
   void collect(RolloutBatch& batch);
-  void step_host(const double* host_logits, int64_t count, float* host_rewards, uint8_t* host_done);
+  void step_host(const double* host_logits, int64_t count, float* host_rewards, uint8_t* host_done,
+                 float* host_obs = nullptr, int64_t obs_count = 0);
+  // Env chunks of the pipelined host step (0 = automatic, ~8 MB of logits each).
+  void set_host_chunks(int32_t n) { host_chunks_ = std::min<int32_t>(std::max<int32_t>(n, 0), kMaxHostChunks); }
   void run(int64_t steps);
   void reduce_stats_into(double* device_out);
   int64_t next_step() const { return t_; }
@@ -251,7 +271,7 @@ class Rollout {
 
  private:
   TagLaunch fused_launch(int64_t step) const;
-  void step_unfused();
+  void step_unfused(float* cap_rewards = nullptr, uint8_t* cap_done = nullptr);
   void forward_policies(cudaStream_t st, int64_t step, const int64_t* step_dev, int32_t step_add,
                         double* values_out, bool force_logits, bool sample);
   bool policy_samples() const { return pol_[0] != nullptr && pol_prec_ == 1; }  // kPolicyBF16
@@ -280,11 +300,20 @@ class Rollout {
   uint32_t* pdl_flags_ = nullptr;  // the store's (DataStore::pdl_flags)
   bool graph_pdl_ = false;         // the captured graph's nodes overlap (PDL)
   void set_pdl(TagLaunch& L, bool single_step) const;
-  // host-driven stepping: double-buffered logits + copy stream
+  void note_launch(const TagLaunch& L);
+  // host-driven stepping: double-buffered logits, H2D and D2H copy streams,
+  // pre-reset rewards / done capture buffers, per-chunk events
+  static constexpr int kMaxHostChunks = 16;
+  int32_t host_chunks_ = 0;
   cudaStream_t copy_ = nullptr;
+  cudaStream_t d2h_ = nullptr;
   double* dlog_[2] = {nullptr, nullptr};
-  cudaEvent_t h2d_done_[2] = {nullptr, nullptr};
-  cudaEvent_t kern_done_[2] = {nullptr, nullptr};
+  cudaEvent_t slot_free_[2] = {nullptr, nullptr};
+  cudaEvent_t h2d_ev_[kMaxHostChunks] = {};
+  cudaEvent_t kern_ev_[kMaxHostChunks] = {};
+  cudaEvent_t d2h_ev_ = nullptr;
+  float* rew_cap_ = nullptr;
+  uint8_t* done_cap_ = nullptr;
   // CUDA-graph replay of kGraphSteps fused launches (run()).
   void build_graph();
   void drop_graph();
@@ -322,5 +351,7 @@ inline constexpr uint64_t kStreamActions = 0x616374696f6e7331ULL;
 inline constexpr uint64_t kStreamPlacement = 0x706c6163656d656eULL;
 
 float& fault_tag_radius_bias();
+// Plan tuning overrides (tag.cpp kTuningKeys); "reset" restores the defaults.
+void set_tuning(const std::string& key, int64_t value);
 
 }  // namespace wdg

@@ -723,9 +723,11 @@ void Policy::forward_sample_bf16(const float* obs, int64_t E, int64_t A, int64_t
   const int by_regs = 65536 / std::max(1, fa.numRegs * kBfThreads);
   const int by_smem = smem_sm / (smem + static_cast<int>(fa.sharedSizeBytes) + 1024);
   per_sm = std::max(1, std::min({by_regs, by_smem, 512 / kBfTmemCols}));
+#ifdef WDG_TUNING
   if (std::getenv("WDG_DEBUG_POLICY")) {
     std::fprintf(stderr, "policy bf16: regs %d smem %d -> %d CTAs/SM\n", fa.numRegs, smem, per_sm);
   }
+#endif
   const int64_t tiles = (E * b.n + kBfRows - 1) / kBfRows;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t{sms} * per_sm)));
   b.pdl = pdl ? 1 : 0;

@@ -53,6 +53,17 @@ uint32_t* DataStore::pdl_flags() {
   return pdl_flags_;
 }
 
+void DataStore::reset_pdl() {
+  // Only after a synchronize (no launch in flight): every flag back to 0 and
+  // the next launch waits for sequence 0, which every env now shows.
+  if (pdl_flags_ != nullptr) {
+    cuda_check(cudaMemset(pdl_flags_, 0, static_cast<size_t>(num_envs_) * sizeof(uint32_t)),
+               "memset(pdl flags)");
+  }
+  pdl_seq_ = 0;
+  pdl_open_ = false;
+}
+
 void DataStore::set_env_offset(int64_t off) {
   if (off < 0) raise(Errc::invalid_argument, "set_env_offset: offset must be >= 0");
   env_offset_ = off;

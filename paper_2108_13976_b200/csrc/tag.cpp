@@ -31,6 +31,63 @@ float& fault_tag_radius_bias() {
   return bias;
 }
 
+// ---- plan tuning overrides --------------------------------------------------
+// Geometry / launch-overlap choices the plan normally makes itself, settable
+// through wdg_set_tuning for A/B measurements and for tests that pin a code
+// path. None of them changes WHAT a launch computes, only how it is mapped.
+// Environment variables are read only by a tuning build (-DWDG_TUNING).
+namespace {
+struct TuningKey {
+  const char* name;
+  const char* env;
+};
+constexpr TuningKey kTuningKeys[] = {
+    {"stage_rows", "WDG_STAGE_ROWS"},             // 16 / 32: continuous K=5 obs staging rows per pass
+    {"brute_max", "WDG_BRUTE_MAX"},               // agents up to which the brute-force layout is used
+    {"threads_per_env_max", "WDG_TPE_MAX"},       // CTA thread cap of the one-env-per-CTA layout
+    {"cont_cell_div", "WDG_CONT_GC_DIV"},         // continuous: agents per bucket cell
+    {"disc_grid_cells", "WDG_DISC_GC"},           // discrete: bucket cells per side
+    {"stage_obs", "WDG_STAGE_OBS"},               // 0: never stage observation rows in smem
+    {"bulk_in", "WDG_BULK_IN"},                   // 0: no TMA bulk staging of the inputs
+    {"l2_prefetch", "WDG_L2_PREFETCH"},           // env stride of an L2 prefetch of later inputs
+    {"pdl_mode", "WDG_PDL"},                      // launch overlap, TagPlan::pdl_mode values
+    {"multistep", "WDG_MULTISTEP"},               // 0: no multi-step residency in run()
+};
+constexpr int kNumTuning = static_cast<int>(sizeof(kTuningKeys) / sizeof(kTuningKeys[0]));
+int64_t* tuning_table() {
+  static int64_t table[kNumTuning] = {};
+  static bool init = [] {
+    for (int i = 0; i < kNumTuning; ++i) table[i] = -1;
+#ifdef WDG_TUNING
+    for (int i = 0; i < kNumTuning; ++i)
+      if (const char* v = std::getenv(kTuningKeys[i].env)) table[i] = std::atoll(v);
+#endif
+    return true;
+  }();
+  (void)init;
+  return table;
+}
+int64_t tuning(const char* name, int64_t fallback) {
+  for (int i = 0; i < kNumTuning; ++i)
+    if (std::string(kTuningKeys[i].name) == name) return tuning_table()[i] >= 0 ? tuning_table()[i] : fallback;
+  return fallback;
+}
+}  // namespace
+
+void set_tuning(const std::string& key, int64_t value) {
+  if (key == "reset") {
+    for (int i = 0; i < kNumTuning; ++i) tuning_table()[i] = -1;
+    return;
+  }
+  for (int i = 0; i < kNumTuning; ++i) {
+    if (key == kTuningKeys[i].name) {
+      tuning_table()[i] = value < 0 ? -1 : value;
+      return;
+    }
+  }
+  raise(Errc::invalid_argument, "set_tuning: unknown key \"" + key + "\"");
+}
+
 // ---- TagConfig::validate (tag_env.cpp:20-40) -------------------------------
 void validate_tag_config(const wdg_tag_config& c) {
   auto fail = [](const std::string& msg) { raise(Errc::invalid_config, "TagConfig: " + msg); };
@@ -102,9 +159,10 @@ int resident_ctas(const TagDevConfig& p) {
 TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) {
   TagDevConfig full = make_dev_config_rows(store, cfg, 32);
   if (!full.continuous || !full.partial || full.K != 5 || !full.use_grid || !full.stage_obs) return full;
-  if (std::getenv("WDG_STAGE_FULL_WARP") != nullptr) return full;
+  const int64_t forced = tuning("stage_rows", 0);
+  if (forced == 32) return full;
   TagDevConfig half = make_dev_config_rows(store, cfg, 16);
-  if (std::getenv("WDG_STAGE_HALF_WARP") != nullptr) return half;  // tuning experiments only
+  if (forced == 16) return half;
   return resident_ctas(half) > resident_ctas(full) ? half : full;
 }
 
@@ -170,7 +228,7 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   int brute_max = !p.partial ? kBruteMaxAgents
                   : p.continuous ? kBruteMaxPartialCont
                   : lattice_fits ? kBruteMaxAgents : kBruteMaxPartialDisc;
-  if (const char* env = std::getenv("WDG_BRUTE_MAX")) brute_max = std::atoi(env);  // tuning experiments only
+  brute_max = static_cast<int>(tuning("brute_max", brute_max));
   brute_max = std::min(brute_max, kMaxThreadsPerCta);  // one thread per agent of a packed env
   p.use_grid = A > brute_max ? 1 : 0;
   if (p.use_grid) {
@@ -185,7 +243,7 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     int cap = 256;
     if (p.partial && (p.continuous ? A <= 400 : A <= 512)) cap = 128;
     else if (p.partial && !p.continuous && A <= 864) cap = 192;
-    if (const char* env = std::getenv("WDG_TPE_MAX")) cap = std::clamp(std::atoi(env), 32, 1024) / 32 * 32;
+    if (const int64_t t = tuning("threads_per_env_max", 0)) cap = static_cast<int>(std::clamp<int64_t>(t, 32, 1024)) / 32 * 32;
     cap = std::min(cap, kMaxThreadsPerCta);
     p.envs_per_cta = 1;
     p.threads = std::min<int32_t>(round_up(A, 32), cap);
@@ -216,15 +274,15 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     // (fewer cells per query). Measured at A = 100 / 1000: 1 agent per cell
     // 128 / 537 us/step, 2: 107 / 467, 3: 101 / 446, 4: 101 / 451.
     int div = 3;
-    if (const char* env = std::getenv("WDG_CONT_GC_DIV")) div = std::max(1, std::atoi(env));
+    div = static_cast<int>(std::max<int64_t>(1, tuning("cont_cell_div", div)));
     p.gc = std::max(1, std::min(static_cast<int>(std::floor(std::sqrt(static_cast<double>(A) / div))), 128));
     p.cell_inv = static_cast<float>(static_cast<double>(p.gc) / cfg.world_length);
     p.cell_size = cfg.world_length / p.gc;
   } else {
     p.gc = static_cast<int32_t>(std::min<int64_t>(cfg.grid_size, std::min(sq, 128)));
     if (lattice_fits) p.gc = static_cast<int32_t>(g);
-    if (const char* env = std::getenv("WDG_DISC_GC"))  // tuning experiments only
-      p.gc = static_cast<int32_t>(std::clamp<int64_t>(std::atoi(env), 1, std::min<int64_t>(cfg.grid_size, 128)));
+    if (const int64_t t = tuning("disc_grid_cells", 0))
+      p.gc = static_cast<int32_t>(std::clamp<int64_t>(t, 1, std::min<int64_t>(cfg.grid_size, 128)));
     p.lattice_w = static_cast<int32_t>(cfg.grid_size / p.gc);
     p.lattice = p.gc == cfg.grid_size ? 1 : 0;
   }
@@ -233,7 +291,7 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   const int64_t nwarps = p.threads / 32;
   int64_t stage_bytes = nwarps * 32 * int64_t{p.D} * 4;
   p.stage_obs = (p.D <= 64 && stage_bytes <= 112 * 1024) ? 1 : 0;
-  if (const char* env = std::getenv("WDG_STAGE_OBS")) p.stage_obs = p.stage_obs && std::atoi(env) != 0;
+  p.stage_obs = p.stage_obs && tuning("stage_obs", 1) != 0;
   // Continuous K=5 rows (D = 41) at one env per CTA may use half-warp passes
   // (see make_dev_config): the staging buffer halves (42 -> 21 KB at 256 threads).
   p.stage_rows = 32;
@@ -292,7 +350,7 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   // zone starts at the first late array (CTA offset head + late_begin) and grows
   // the CTA's smem if the logits need more than those areas.
   p.bulk_in = 0;
-  if (p.use_grid && (A % 4) == 0 && std::getenv("WDG_NO_BULK") == nullptr) {
+  if (p.use_grid && (A % 4) == 0 && tuning("bulk_in", 1) != 0) {
     const int64_t logits_bytes = int64_t{A} * p.C * p.V * 8;
     const int64_t zone = align16(static_cast<int64_t>(p.head_bytes) + late_begin);
     const int64_t need = zone + logits_bytes;
@@ -300,11 +358,10 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
       p.bulk_in = 1;
       p.off_zone = static_cast<int32_t>(zone);
       total = std::max<int64_t>(total, need);
-      // Optional L2 prefetch of the next wave's env inputs (WDG_L2_PREFETCH =
-      // env stride). Off: measured neutral at one wave (296) and -3% at
-      // 592 / 1184 envs ahead on C2 — the bulk loads are not HBM-bound.
-      p.prefetch_stride = 0;
-      if (const char* env = std::getenv("WDG_L2_PREFETCH")) p.prefetch_stride = std::atoi(env);
+      // Optional L2 prefetch of the next wave's env inputs (tuning key
+      // l2_prefetch = env stride). Off: measured neutral at one wave (296)
+      // and -3% at 592 / 1184 envs ahead on C2 — the bulk loads are not HBM-bound.
+      p.prefetch_stride = static_cast<int32_t>(tuning("l2_prefetch", 0));
     }
   }
   if (total > kMaxSmem) {
@@ -437,7 +494,7 @@ void TagPlan::launch(TagLaunch L) {
 //   kernels can overlap. Plain PDL (release at entry, whole-grid
 //   griddepcontrol.wait) still hides the launch gap there: 6.9 vs 8.2.
 int TagPlan::pdl_mode() const {
-  if (const char* env = std::getenv("WDG_PDL")) return std::atoi(env);  // A/B experiments
+  if (const int64_t t = tuning("pdl_mode", -1); t >= 0) return static_cast<int>(t);  // A/B experiments, tests
   if (!dev_.use_grid) return (dev_.envs_per_cta <= 4 && dev_.threads >= 128) ? 1 : 3;
   if (!dev_.continuous && dev_.partial && dev_.threads < 256) return 2;
   return 1;
@@ -468,6 +525,48 @@ bool TagPlan::multistep_ok() {
     }
   }
   return multistep_ == 1;
+}
+
+// One launch over the env range [e0, e0 + n): the plan's geometry with every
+// per-env pointer moved to env e0 and env_offset advanced, so the RNG keys
+// (global env ids) and the results equal those of a whole-store launch.
+void TagPlan::launch_envs(TagLaunch L, int64_t e0, int64_t n) {
+  if (e0 == 0 && n == dev_.E) return launch(L);
+  if (e0 < 0 || n <= 0 || e0 + n > dev_.E) raise(Errc::index_out_of_range, "tag launch: env range");
+  TagDevConfig d = dev_;
+  d.fault_bias = fault_tag_radius_bias();
+  d.E = static_cast<int32_t>(n);
+  d.env_offset += e0;
+  d.grid_ctas = static_cast<int32_t>((n + d.envs_per_cta - 1) / d.envs_per_cta);
+  const int64_t A = d.A;
+  TagDevArrays g = arrays_;
+  auto adv = [&](auto*& ptr, int64_t per_env) {
+    if (ptr != nullptr) ptr += e0 * per_env;
+  };
+  adv(g.loc_x, A);
+  adv(g.loc_y, A);
+  adv(g.speed, A);
+  adv(g.direction, A);
+  adv(g.obs, A * d.D);
+  adv(g.rewards, A);
+  adv(g.is_tagger, A);
+  adv(g.active, A);
+  adv(g.tagged, A);
+  adv(g.done, 1);
+  adv(g.step_count, 1);
+  adv(g.actions, A * d.C);
+  adv(g.credits, A);
+  adv(g.snap_is_tagger, A);
+  adv(L.logits, A * d.C * d.V);
+  adv(L.env_mask, 1);
+  adv(L.episode, 1);
+  adv(L.env_stats, 8);
+  adv(L.cap_actions, A * d.C);
+  adv(L.cap_active, A);
+  adv(L.cap_rewards, A);
+  adv(L.cap_done, 1);
+  adv(L.env_seq, 1);
+  cuda_check(launch_tag_kernel(d, g, L, store_.stream()), "tag kernel launch (env range)");
 }
 
 void TagPlan::run_step(int64_t step_index) {
@@ -659,8 +758,7 @@ Rollout::Rollout(DataStore& store, TagPlan& plan, ResetManager* resets, uint64_t
   }
   logits_ = zero_logits_;
   h_actions0_ = host_mix64(host_substream(seed_, kStreamActions));
-  // WDG_NO_PDL (A/B timing and tests): one plain launch per step
-  if (std::getenv("WDG_NO_PDL") == nullptr) pdl_flags_ = store_.pdl_flags();
+  pdl_flags_ = store_.pdl_flags();  // set_overlap(false): one plain launch per step
 }
 
 Rollout::~Rollout() {
@@ -668,10 +766,17 @@ Rollout::~Rollout() {
   if (step_dev_) cudaFree(step_dev_);
   for (int i = 0; i < 2; ++i) {
     if (dlog_[i]) cudaFree(dlog_[i]);
-    if (h2d_done_[i]) cudaEventDestroy(h2d_done_[i]);
-    if (kern_done_[i]) cudaEventDestroy(kern_done_[i]);
+    if (slot_free_[i]) cudaEventDestroy(slot_free_[i]);
   }
+  for (int i = 0; i < kMaxHostChunks; ++i) {
+    if (h2d_ev_[i]) cudaEventDestroy(h2d_ev_[i]);
+    if (kern_ev_[i]) cudaEventDestroy(kern_ev_[i]);
+  }
+  if (d2h_ev_) cudaEventDestroy(d2h_ev_);
+  if (rew_cap_) cudaFree(rew_cap_);
+  if (done_cap_) cudaFree(done_cap_);
   if (copy_) cudaStreamDestroy(copy_);
+  if (d2h_) cudaStreamDestroy(d2h_);
   if (zero_logits_) cudaFree(zero_logits_);
   if (pol_logits_) cudaFree(pol_logits_);
   if (pol_values_) cudaFree(pol_values_);
@@ -679,6 +784,12 @@ Rollout::~Rollout() {
   if (stats_) cudaFree(stats_);
   if (error_) cudaFree(error_);
   if (own_episode_) cudaFree(own_episode_);
+}
+
+void Rollout::set_overlap(bool enabled) {
+  uint32_t* want = enabled ? store_.pdl_flags() : nullptr;
+  if (want != pdl_flags_) drop_graph();  // captured with or without overlapped nodes
+  pdl_flags_ = want;
 }
 
 void Rollout::set_logits(const double* logits, int64_t count) {
@@ -714,12 +825,15 @@ TagLaunch Rollout::fused_launch(int64_t step) const {
   L.episode = resets_ ? resets_->episode_device() : own_episode_;
   L.env_stats = env_stats_;
   L.error = error_;
-  // Performance-analysis ablation (results invalid); see TagLaunch::ablate.
+#ifdef WDG_TUNING
+  // Performance-analysis ablation (results invalid; tuning builds only, the
+  // product kernel ignores TagLaunch::ablate).
   static const uint32_t ablate = [] {
     const char* v = std::getenv("WDG_ABLATE");
     return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 0)) : 0u;
   }();
   L.ablate = ablate;
+#endif
   return L;
 }
 
@@ -780,13 +894,14 @@ void Rollout::forward_policies(cudaStream_t st, int64_t step, const int64_t* ste
     k.step_add = step_add;
     k.h0 = h_actions0_;
     int32_t* act = sample ? static_cast<int32_t*>(store_.device_ptr(store_.handle(kSampledActions))) : nullptr;
-    const bool pdl = pdl_flags_ != nullptr;  // WDG_NO_PDL off switch
+    const bool pdl = pdl_flags_ != nullptr;  // set_overlap(false) off switch
     if (pol_[0] == pol_[1]) {
       pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.A, act, lg, vl, k, st, error_, pdl);
     } else {
       pol_[0]->forward_sample_bf16(obs, p.E, p.A, 0, p.T, act, lg, vl, k, st, error_, pdl);
       pol_[1]->forward_sample_bf16(obs, p.E, p.A, p.T, p.A, act, lg, vl, k, st, error_, pdl);
     }
+    if (pdl && step_dev == nullptr) store_.set_pdl_open(true);  // released at entry, no env flags
     return;
   }
   if (pol_[0] == pol_[1]) {
@@ -830,7 +945,7 @@ void Rollout::collect(RolloutBatch& b) {
   forward_policies(st, t_, nullptr, 0, b.bootstrap, true, false);
 }
 
-void Rollout::step_unfused() {
+void Rollout::step_unfused(float* cap_rewards, uint8_t* cap_done) {
   const TagDevConfig& p = plan_.dev();
   const uint64_t h_step = host_absorb(h_actions0_, static_cast<uint64_t>(t_));
   if (!policy_samples()) cuda_check(launch_sample(logits_,
@@ -839,7 +954,19 @@ void Rollout::step_unfused() {
                            store_.stream()),
              "sample kernel");
   plan_.run_step(t_);
+  if (cap_rewards != nullptr) {  // before reset-on-done zeroes them
+    cuda_check(cudaMemcpyAsync(cap_rewards, store_.device_ptr(store_.handle(kRewards)),
+                               static_cast<size_t>(p.E) * p.A * sizeof(float), cudaMemcpyDeviceToDevice,
+                               store_.stream()),
+               "capture rewards");
+  }
+  if (cap_done != nullptr) {
+    cuda_check(cudaMemcpyAsync(cap_done, store_.device_ptr(store_.handle(kDone)), static_cast<size_t>(p.E),
+                               cudaMemcpyDeviceToDevice, store_.stream()),
+               "capture done");
+  }
   if (resets_ != nullptr && resets_->auto_enabled()) resets_->auto_reset_on_done();
+  store_.set_pdl_open(false);  // plain launches: each waits for its predecessor to finish
   launches_ += policy_samples() ? 1 : 2;  // (+ the reset kernels, counted in the ResetManager's own launches)
 }
 
@@ -867,6 +994,16 @@ void Rollout::set_pdl(TagLaunch& L, bool single_step) const {
   L.env_seq = pdl_flags_;
   L.seq = store_.pdl_seq() + 1u;
   L.pdl_late = mode == 2 ? 1 : 0;
+  // The previous kernel released this launch early without publishing flags
+  // (bf16 policy step, collect's bootstrap forward): wait for all of it first.
+  if (store_.pdl_open()) L.pdl_wait = 1;
+}
+
+// After a Tag launch: did it release its dependents without publishing env
+// flags (DataStore::pdl_open)?
+void Rollout::note_launch(const TagLaunch& L) {
+  if (L.env_seq != nullptr) store_.commit_pdl_seq();
+  store_.set_pdl_open(L.env_seq == nullptr && L.pdl_wait != 0);
 }
 
 void Rollout::step() {
@@ -875,7 +1012,7 @@ void Rollout::step() {
     TagLaunch L = fused_launch(t_);
     set_pdl(L, true);
     plan_.launch(L);
-    if (L.env_seq != nullptr) store_.commit_pdl_seq();
+    note_launch(L);
     ++launches_;
   } else {
     step_unfused();
@@ -883,52 +1020,117 @@ void Rollout::step() {
   ++t_;
 }
 
+// Host-driven step (the drop-in host integration): what a host learner reads
+// after RolloutDriver::step — the step's rewards and done captured BEFORE
+// reset-on-done (Trainer::collect post_step, trainer.cpp:382-394, ahead of
+// auto_reset, harness.cpp:478-490) and, optionally, the observations after it
+// (post-reset: what the next policy_forward reads, trainer.cpp:358-360).
+// The step is pipelined over env chunks on three streams: the H2D of chunk
+// g + 1's logits, the fused kernel of chunk g and the D2H of chunk g - 1's
+// outputs overlap (PCIe is full duplex), so a closed-loop step costs about
+// max(H2D, D2H) instead of their sum. Every chunk uses the step's index and
+// global env ids, so the results equal one whole-store launch.
 void Rollout::step_host(const double* host_logits, int64_t count, float* host_rewards,
-                        uint8_t* host_done) {
+                        uint8_t* host_done, float* host_obs, int64_t obs_count) {
   const TagDevConfig& p = plan_.dev();
-  const int64_t expected = int64_t{p.E} * p.A * p.C * p.V;
+  const int64_t per_env_logits = int64_t{p.A} * p.C * p.V;
+  const int64_t expected = int64_t{p.E} * per_env_logits;
   if (host_logits == nullptr) raise(Errc::invalid_argument, "step_host: null logits");
   if (pol_[0] != nullptr) raise(Errc::state_error, "step_host: the rollout samples from device policies");
   if (count != expected) {
     raise(Errc::shape_mismatch, "step_host: logits size " + std::to_string(count) + ", expected " +
                                     std::to_string(expected));
   }
+  if (host_obs != nullptr && obs_count != int64_t{p.E} * p.A * p.D) {
+    raise(Errc::shape_mismatch, "step_host: observations size " + std::to_string(obs_count) +
+                                    ", expected " + std::to_string(int64_t{p.E} * p.A * p.D));
+  }
   const size_t bytes = static_cast<size_t>(expected) * sizeof(double);
   if (copy_ == nullptr) {
     cuda_check(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
+    cuda_check(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "d2h stream");
     for (int i = 0; i < 2; ++i) {
       cuda_check(cudaMalloc(&dlog_[i], bytes), "cudaMalloc(logits slot)");
-      cuda_check(cudaEventCreateWithFlags(&h2d_done_[i], cudaEventDisableTiming), "event");
-      cuda_check(cudaEventCreateWithFlags(&kern_done_[i], cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&slot_free_[i], cudaEventDisableTiming), "event");
     }
+    for (int i = 0; i < kMaxHostChunks; ++i) {
+      cuda_check(cudaEventCreateWithFlags(&h2d_ev_[i], cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&kern_ev_[i], cudaEventDisableTiming), "event");
+    }
+    cuda_check(cudaEventCreateWithFlags(&d2h_ev_, cudaEventDisableTiming), "event");
+    cuda_check(cudaMalloc(&rew_cap_, static_cast<size_t>(p.E) * p.A * sizeof(float)), "cudaMalloc(rewards capture)");
+    cuda_check(cudaMalloc(&done_cap_, static_cast<size_t>(p.E)), "cudaMalloc(done capture)");
   }
+  const bool fused = fused_ok();
+  // Chunks: ~8 MB of logits each (C2: 8 chunks of 250 envs), whole CTAs.
+  int chunks = host_chunks_ > 0 ? host_chunks_
+                                : static_cast<int>(std::clamp<int64_t>(static_cast<int64_t>(bytes >> 23), 1, kMaxHostChunks));
+  if (!fused) chunks = 1;
+  const int64_t epc = p.envs_per_cta;
+  const int64_t per = (int64_t{p.E} + chunks - 1) / chunks;
+  const int64_t per_chunk = std::max<int64_t>(epc, (per + epc - 1) / epc * epc);
   const int slot = static_cast<int>(t_ & 1);
   cudaStream_t st = store_.stream();
-  // The slot was last read by the kernel of step t-2.
-  cuda_check(cudaStreamWaitEvent(copy_, kern_done_[slot], 0), "wait kernel");
-  cuda_check(cudaMemcpyAsync(dlog_[slot], host_logits, bytes, cudaMemcpyHostToDevice, copy_), "H2D logits");
-  cuda_check(cudaEventRecord(h2d_done_[slot], copy_), "record h2d");
-  cuda_check(cudaStreamWaitEvent(st, h2d_done_[slot], 0), "wait h2d");
-  const double* saved = logits_;
-  logits_ = dlog_[slot];
-  try {
-    step();
-  } catch (...) {
-    logits_ = saved;
-    throw;
+  // The slot was last read by the kernels of step t-2.
+  cuda_check(cudaStreamWaitEvent(copy_, slot_free_[slot], 0), "wait slot");
+  int g = 0;
+  for (int64_t e0 = 0; e0 < p.E; e0 += per_chunk, ++g) {
+    const int64_t n = std::min<int64_t>(per_chunk, p.E - e0);
+    cuda_check(cudaMemcpyAsync(dlog_[slot] + e0 * per_env_logits, host_logits + e0 * per_env_logits,
+                               static_cast<size_t>(n * per_env_logits) * sizeof(double),
+                               cudaMemcpyHostToDevice, copy_),
+               "H2D logits");
+    cuda_check(cudaEventRecord(h2d_ev_[g], copy_), "record h2d");
   }
-  logits_ = saved;
-  cuda_check(cudaEventRecord(kern_done_[slot], st), "record kernel");
-  if (host_rewards) {
-    cuda_check(cudaMemcpyAsync(host_rewards, store_.device_ptr(store_.handle(kRewards)),
-                               static_cast<size_t>(p.E) * p.A * sizeof(float), cudaMemcpyDeviceToHost, st),
-               "D2H rewards");
+  g = 0;
+  for (int64_t e0 = 0; e0 < p.E; e0 += per_chunk, ++g) {
+    const int64_t n = std::min<int64_t>(per_chunk, p.E - e0);
+    cuda_check(cudaStreamWaitEvent(st, h2d_ev_[g], 0), "wait h2d");
+    if (fused) {
+      TagLaunch L = fused_launch(t_);
+      L.logits = dlog_[slot];
+      L.cap_rewards = rew_cap_;
+      L.cap_done = done_cap_;
+      plan_.launch_envs(L, e0, n);  // plain launch: waits for its stream predecessors
+      ++launches_;
+    } else {
+      const double* saved = logits_;
+      logits_ = dlog_[slot];
+      try {
+        step_unfused(rew_cap_, done_cap_);
+      } catch (...) {
+        logits_ = saved;
+        throw;
+      }
+      logits_ = saved;
+    }
+    cuda_check(cudaEventRecord(kern_ev_[g], st), "record kernel");
+    cuda_check(cudaStreamWaitEvent(d2h_, kern_ev_[g], 0), "wait kernel");
+    if (host_rewards) {
+      cuda_check(cudaMemcpyAsync(host_rewards + e0 * p.A, rew_cap_ + e0 * p.A,
+                                 static_cast<size_t>(n * p.A) * sizeof(float), cudaMemcpyDeviceToHost, d2h_),
+                 "D2H rewards");
+    }
+    if (host_done) {
+      cuda_check(cudaMemcpyAsync(host_done + e0, done_cap_ + e0, static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                                 d2h_),
+                 "D2H done");
+    }
+    if (host_obs) {
+      const int64_t row = int64_t{p.A} * p.D;
+      const float* obs = static_cast<const float*>(store_.device_ptr(store_.handle(kObservations)));
+      cuda_check(cudaMemcpyAsync(host_obs + e0 * row, obs + e0 * row, static_cast<size_t>(n * row) * sizeof(float),
+                                 cudaMemcpyDeviceToHost, d2h_),
+                 "D2H observations");
+    }
   }
-  if (host_done) {
-    cuda_check(cudaMemcpyAsync(host_done, store_.device_ptr(store_.handle(kDone)),
-                               static_cast<size_t>(p.E), cudaMemcpyDeviceToHost, st),
-               "D2H done");
-  }
+  cuda_check(cudaEventRecord(slot_free_[slot], st), "record slot");
+  // The store stream waits for the copies: wdg_store_synchronize covers the
+  // outputs, and the next step's kernels (which rewrite them) follow them.
+  cuda_check(cudaEventRecord(d2h_ev_, d2h_), "record d2h");
+  cuda_check(cudaStreamWaitEvent(st, d2h_ev_, 0), "wait d2h");
+  store_.set_pdl_open(false);
+  ++t_;
 }
 
 void Rollout::reduce_stats_into(double* device_out) {
@@ -1001,7 +1203,7 @@ void Rollout::run(int64_t steps) {
   // steps) consecutive steps are independent launches of the same kernel on
   // the same env, so one launch runs up to kMultiSteps of them with each
   // env's state kept in shared memory (TagLaunch::n_steps).
-  const bool multi_off = std::getenv("WDG_NO_MULTISTEP") != nullptr;  // read per run() (A/B timing in one process)
+  const bool multi_off = tuning("multistep", 1) == 0;  // read per run() (A/B timing in one process)
   if (!multi_off && fused_ok() && pol_[0] == nullptr && steps > 1 && plan_.multistep_ok()) {
     while (steps > 0) {
       const int32_t k = static_cast<int32_t>(std::min<int64_t>(steps, kMultiSteps));
@@ -1011,7 +1213,7 @@ void Rollout::run(int64_t steps) {
       L.action_h0 = h_actions0_;
       set_pdl(L, false);  // the next window's early envs start in this one's tail
       plan_.launch(L);
-      if (L.env_seq != nullptr) store_.commit_pdl_seq();
+      note_launch(L);
       ++launches_;
       t_ += k;
       steps -= k;
@@ -1032,6 +1234,7 @@ void Rollout::run(int64_t steps) {
       cuda_check(cudaGraphLaunch(graph_exec_, store_.stream()), "graph launch");
       if (graph_pdl)
         for (int i = 0; i < kGraphSteps; ++i) store_.commit_pdl_seq();
+      store_.set_pdl_open(false);  // the last node is a Tag launch that either publishes or never releases early
       launches_ += 1 + kGraphSteps * (pol_[0] != nullptr ? (pol_[0] == pol_[1] ? 2 : 3) : 1);
       t_ += kGraphSteps;
       steps -= kGraphSteps;
@@ -1051,7 +1254,10 @@ void Rollout::check() {
   }
   if (err & kErrStepOrder) {
     cudaMemsetAsync(error_, 0, sizeof(uint32_t), store_.stream());
-    raise(Errc::cuda, "fused rollout: an overlapped step timed out waiting for the previous step");
+    store_.synchronize();
+    store_.reset_pdl();
+    raise(Errc::cuda, "fused rollout: an overlapped step timed out waiting for the previous step; "
+                      "the affected envs skipped it (state is no longer in lockstep)");
   }
 }
 
@@ -1062,6 +1268,7 @@ void Rollout::stats(double* out, int32_t count) {
              "stats pull");
   store_.synchronize();
   for (int32_t i = 0; i < count && i < WDG_STAT_COUNT; ++i) out[i] = host[i];
+  check();  // surface sticky device errors at this synchronising call
 }
 
 void Rollout::reset_stats() {

@@ -460,6 +460,18 @@ __device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t
 
 // Per-cell top-(K+1) lists for every cell holding an active agent (only those
 // are ever looked up); s.cfill[c] = entries found.
+// Performance-analysis ablation bits (TagLaunch::ablate): only a tuning
+// build (-DWDG_TUNING) reads them; the product build folds them to 0, so no
+// launch of the shipped library can skip work.
+__device__ __forceinline__ uint32_t ablate_bits(const TagLaunch& L) {
+#ifdef WDG_TUNING
+  return L.ablate;
+#else
+  (void)L;
+  return 0u;
+#endif
+}
+
 __device__ __forceinline__ void build_cell_lists(const EnvSmem& s, const TagDevConfig& p, uint32_t ablate) {
   const int kk = p.K + 1;
   for (int c = threadIdx.x; c < p.ncells; c += blockDim.x) {
@@ -1279,9 +1291,17 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   const uint32_t seq = L.seq_dev != nullptr ? static_cast<uint32_t>(*L.seq_dev) + L.seq_add : L.seq;
   if (pdl) {
     if (!L.pdl_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // A wait that gives up (seconds: preemption, a debugger) skips this CTA's
+    // envs for this launch — state untouched, flags not published — and sets
+    // the sticky kErrStepOrder bit; once it is set, later launches skip at
+    // once instead of polling. Rollout::check / stats raise it and resync.
+    bool skip = false;
     if (tid == 0) {
+      uint32_t errw = 0;
+      if (L.error) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(errw) : "l"(L.error) : "memory");
+      skip = (errw & kErrStepOrder) != 0;
       const int64_t eb = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta;
-      for (int k = 0; k < p.envs_per_cta && eb + k < p.E; ++k) {
+      for (int k = 0; !skip && k < p.envs_per_cta && eb + k < p.E; ++k) {
         const uint32_t* f = L.env_seq + eb + k;
         // relaxed polling (an acquire per poll would invalidate this SM's L1
         // under the CTAs still working on it), backing off, then one acquire
@@ -1291,6 +1311,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           if (static_cast<int32_t>(v - (seq - 1u)) >= 0) break;
           if (++polls > (1u << 22)) {  // >= 4 s of polling: report, never hang the device
             if (L.error) atomicOr(L.error, kErrStepOrder);
+            skip = true;
             break;
           }
           __nanosleep(ns);
@@ -1300,7 +1321,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
-    __syncthreads();
+    if (__syncthreads_or(skip)) return;
   }
 
   // Per-env scalars are loaded first (by the env's lane 0) so their latency
@@ -1454,7 +1475,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
             const int a = a0 + P * h + k;
             const uint64_t h_ag = absorb(h_env, static_cast<uint64_t>(a));
             const double u0 = to_unit(absorb(absorb(h_ag, 0), 0));
-            const int32_t s0 = (L.ablate & 1u) ? static_cast<int32_t>(u0 * 5.0)
+            const int32_t s0 = (ablate_bits(L) & 1u) ? static_cast<int32_t>(u0 * 5.0)
                                                : sample_regs<kV>(z + k * kC * kV, u0, nonfinite);
             int32_t s1 = 1;
             if (CONT) {
@@ -1642,7 +1663,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     // Phase 2: bucket grid over post-move positions (NeighborGrid::build).
     // lattice cells are exact positions: lowest-index tagger per cell
     const bool cell_tagger = !CONT && GRID && p.lattice && all_integral && p.fault_bias == 0.0f;
-    if (GRID && !(L.ablate & 8u)) build_grid<CONT>(s, p, scratch, false, cell_tagger);
+    if (GRID && !(ablate_bits(L) & 8u)) build_grid<CONT>(s, p, scratch, false, cell_tagger);
 
     // Phase 3: resolve tags (tag_env.cpp:403-456). Counts are warp-aggregated
     // when the CTA is one env; there "any runner still active" is all
@@ -1757,7 +1778,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         }
       }
       if (PARTIAL && !CONT && GRID && p.lattice && all_integral)
-        build_cell_lists(s, p, L.ablate);
+        build_cell_lists(s, p, ablate_bits(L));
     }
     __syncthreads();
     if (live && lt == 0 && track) {
@@ -1888,7 +1909,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     const bool cell_lists = PARTIAL && lattice_ok;  // GRID => single env per CTA
     const int kk = p.K + 1;
     if (cell_lists && !early_inputs) {
-      build_cell_lists(s, p, L.ablate);
+      build_cell_lists(s, p, ablate_bits(L));
       __syncthreads();
     }
     if constexpr (CONT && EXACT && PARTIAL) {
@@ -1901,7 +1922,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           const bool valid = live && a < A;
           const bool act_a = valid && s.act[a];
           int nb[MAXK];
-          if (act_a && !(L.ablate & 4u)) {
+          if (act_a && !(ablate_bits(L) & 4u)) {
             TopK<MAXK, EXACT> top;
             knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, false, top);
 #pragma unroll
@@ -1914,7 +1935,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
             const bool mine = valid && (lane >> 4) == h;
             if (mine) {
               float* row = stage + (lane & 15) * D;
-              if (L.ablate & 4u) {
+              if (ablate_bits(L) & 4u) {
                 row[0] = static_cast<float>(a);
               } else if (!act_a) {
                 constexpr int kD = MAXK * 7 + 5 + 1;
@@ -1960,7 +1981,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       if (valid) {
         float* row = stage + lane * D;
         const int cl = cell_lists ? s.cellof[a] : 0;
-        if (L.ablate & 4u) {
+        if (ablate_bits(L) & 4u) {
           row[0] = static_cast<float>(a);
         } else if (!s.act[a]) {
           // inactive agent: all-zero row (write_obs_row, tag_env.cpp:169-172)
@@ -2046,7 +2067,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     const bool cell_lists = PARTIAL && lattice_ok;  // GRID => single env per CTA
     const int kk = p.K + 1;
     if (cell_lists && !early_inputs) {
-      build_cell_lists(s, p, L.ablate);
+      build_cell_lists(s, p, ablate_bits(L));
       __syncthreads();
     }
     if (PARTIAL && live) {

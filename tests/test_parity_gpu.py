@@ -558,26 +558,28 @@ def test_off_lattice_state_falls_back_exactly(kw, envs):
           seed=43), 1200),
 ])
 @pytest.mark.parametrize("pdl_mode", ["1", "2", "3"])  # per-env waits, released at entry / exit; plain PDL
-def test_overlapped_steps_equal_serial_steps(kw, envs, pdl_mode, monkeypatch):
+def test_overlapped_steps_equal_serial_steps(kw, envs, pdl_mode):
     """RolloutDriver::step launches consecutive fused steps with programmatic
     dependent launch: a CTA of step t+1 starts once its own envs finished step
     t, inside step t's tail. 100 back-to-back steps (no host sync, resets
     included, several waves of CTAs) must equal the same steps launched one
-    after another without overlap (WDG_NO_PDL)."""
+    after another without overlap (set_overlap(False))."""
     dc, oc = cfg_pair(**kw)
-    monkeypatch.setenv("WDG_PDL", pdl_mode)  # overlap even where the plan would not choose it
-    ws1 = W.Workspace(dc, envs)
-    d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 5)
-    monkeypatch.setenv("WDG_NO_PDL", "1")
-    ws2 = W.Workspace(dc, envs)
-    d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 5)
-    monkeypatch.delenv("WDG_NO_PDL")
-    for _ in range(100):
-        d1.step()
-    d1.run(100)  # graph replays / multi-step windows, overlapped
-    for _ in range(100):
-        d2.step()
-    d2.run(100)
+    W.set_tuning("pdl_mode", int(pdl_mode))  # overlap even where the plan would not choose it
+    try:
+        ws1 = W.Workspace(dc, envs)
+        d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 5)
+        ws2 = W.Workspace(dc, envs)
+        d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 5)
+        d2.set_overlap(False)
+        for _ in range(100):
+            d1.step()
+        d1.run(100)  # graph replays / multi-step windows, overlapped
+        for _ in range(100):
+            d2.step()
+        d2.run(100)
+    finally:
+        W.set_tuning("reset")
     names = list(O.array_layout(oc, envs).keys())
     d = O.first_divergence(dev_snapshot(ws1, names), dev_snapshot(ws2, names))
     assert d is None, f"overlapped vs serial steps: first divergence {d}"

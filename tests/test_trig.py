@@ -118,7 +118,7 @@ def test_continuous_multistep_equals_single_steps(name):
 
 
 @pytest.mark.gpu
-def test_continuous_half_warp_staging_bit_exact(monkeypatch):
+def test_continuous_half_warp_staging_bit_exact():
     """Wide continuous rows staged by half-warps (chosen automatically when it
     fits more CTAs per SM, as at A = 1000; forced here at A = 300): bit-exact."""
     torch = pytest.importorskip("torch")
@@ -129,9 +129,11 @@ def test_continuous_half_warp_staging_bit_exact(monkeypatch):
     kw, envs = CONT["cont_part_3x300"]
     oc = O.make_config(**{**kw, "episode_length": 25})
     dc = W.TagConfig(**{f: getattr(oc, f) for f, _ in O.TagConfigC._fields_})
-    monkeypatch.setenv("WDG_STAGE_HALF_WARP", "1")
-    ws = W.Workspace(dc, envs)
-    monkeypatch.delenv("WDG_STAGE_HALF_WARP")
+    W.set_tuning("stage_rows", 16)
+    try:
+        ws = W.Workspace(dc, envs)
+    finally:
+        W.set_tuning("reset")
     drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, oc.seed)
     o = O.OracleWorld(oc, envs)
     for t in range(40):
@@ -140,9 +142,11 @@ def test_continuous_half_warp_staging_bit_exact(monkeypatch):
         d = O.first_divergence({n: ws.store.pull(n) for n in o.layout}, o.snapshot())
         assert d is None, f"half-warp staging step {t}: first divergence {d}"
     ws2 = W.Workspace(dc, envs)  # multi-step windows on the same plan choice
-    monkeypatch.setenv("WDG_STAGE_HALF_WARP", "1")
-    ws3 = W.Workspace(dc, envs)
-    monkeypatch.delenv("WDG_STAGE_HALF_WARP")
+    W.set_tuning("stage_rows", 16)
+    try:
+        ws3 = W.Workspace(dc, envs)
+    finally:
+        W.set_tuning("reset")
     d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 4)
     d3 = W.RolloutDriver(ws3.store, ws3.plan, ws3.resets, 4)
     d2.run(50)
