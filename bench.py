@@ -22,11 +22,16 @@ only the episode-statistics all-reduce every --stats-every steps.
 value  = env-steps/s with state resident in HBM, device-timed (CUDA events on
          the store's stream, max over ranks).
 e2e    = the same metric through the C-ABI host-buffer entry point
-         (wdg_rollout_step_host): each step copies its f64 logits from pinned
-         host memory to the device and reads rewards+done back.
+         (wdg_rollout_step_host), CLOSED LOOP: every step uploads its f64
+         logits from pinned host memory, runs, and reads back the step's
+         rewards and done (as they were before reset-on-done, what a host
+         learner's post_step reads); the host waits for them and consumes them
+         before the next step. `e2e_with_obs` also reads the post-reset
+         observations back every step; `e2e_open_loop` issues the steps
+         without per-step host waits (upload of t+1 overlapping step t).
 --impl reference: the reference's own CPU path (oracle/_ref, compiled from the
-reference sources) on all host cores, sharded into race-free single-worker
-worlds; rank 0 only.
+reference sources) on all host cores over the same 2000 envs, sharded into
+race-free single-worker worlds; rank 0 only.
 """
 import argparse
 import json
@@ -36,6 +41,10 @@ import subprocess
 import sys
 import threading
 import time
+
+import faulthandler
+
+faulthandler.enable()  # a native crash prints the Python stack to stderr
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -60,35 +69,67 @@ def env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms; only samples
-    taken while `active` (a timed region) count."""
+    """SM clocks and throttle reasons DURING timed regions: a background
+    thread samples every 20 ms through NVML (nvidia-smi every 200 ms if NVML is
+    missing) while `active`, and sample_now() takes a synchronous sample (the
+    bench calls it right after enqueueing each timed window, while the GPU is
+    still working through it)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
+    SMI_FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index):
+        # NVML indexes physical GPUs: map through CUDA_VISIBLE_DEVICES
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if ids and all(v.isdigit() for v in ids) and gpu_index < len(ids):
+            gpu_index = int(ids[gpu_index])
         self.gpu = gpu_index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, [reasons])
         self.active = False
         self._stop = False
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(gpu_index))
+        except Exception:
+            self._nvml = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def start(self):
         self._t.start()
         return self
 
+    def _read(self):
+        if self._nvml is not None:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return float(sm), float(mx), [n for n, b in self.REASONS if bits & b]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.SMI_FIELDS}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        return float(f[0]), float(f[1]), [names[i] for i in range(4) if f[2 + i].lower() == "active"]
+
+    def sample_now(self):
+        try:
+            self.samples.append(self._read())
+        except Exception:
+            pass
+
     def _run(self):
+        period = 0.02 if self._nvml is not None else 0.2
         while not self._stop:
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out and self.active:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            time.sleep(0.2)
+            if self.active:
+                self.sample_now()
+            time.sleep(period)
 
     def stop(self):
         self._stop = True
@@ -96,13 +137,10 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted({r for s in self.samples for r in s[2]}),
+                "samples": len(self.samples), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def measured_peak_hbm():
@@ -127,6 +165,10 @@ def ncu_traffic(config_key):
 
 
 # ---- reference arm ----------------------------------------------------------------
+def host_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -134,31 +176,27 @@ def run_reference(args, rank, world):
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libwarpref.so not built"}))
         return 0
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    threads = host_threads()
     cfg = O.make_config(**C2)
-    envs_per_thread = args.ref_envs_per_thread
-    per_step = []
-    setup_total = 0.0
-    # each "step" of this arm = a bounded sample of the workload: every thread
-    # advances its own envs_per_thread-env world by --ref-inner steps.
-    sps, setup, run_s = O.bench_reference_sharded(cfg, envs_per_thread, threads, args.warmup,
-                                                  args.ref_inner * args.steps)
-    setup_total += setup
+    # Every step = one RolloutDriver::step of all ENVS_PER_GPU envs (the same
+    # 2000 x 1000 workload as our arm), split into one race-free
+    # single-worker world per host thread.
+    sps, setup, run_s = O.bench_reference_total(cfg, ENVS_PER_GPU, threads, args.warmup, args.steps)
     value = sps
-    ms_per_step = 1e3 * ENVS_PER_GPU / value  # one 2000-env step at this rate
     line = {
         "impl": "reference",
         "metric": "env-steps/sec (Tag, 2000 envs x 1000 agents)",
         "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": 1e3 * ENVS_PER_GPU / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (env) / f64 (sampler)", "data": "synthetic",
         "config": {"workload": "C2: discrete Tag, partial obs K=5, 2000 envs x 1000 agents "
-                               "(200 taggers), zero logits", "parallelism": f"cpu x{threads}"},
+                               "(200 taggers), zero logits", "envs_total": ENVS_PER_GPU,
+                   "parallelism": f"cpu x{threads}"},
         "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": threads, "kind": "reference",
-                         "sample": f"{threads} threads x {envs_per_thread} envs x 1000 agents, "
-                                   f"{args.ref_inner * args.steps} steps after {args.warmup} warm-up "
-                                   f"(reference StepEngine worker_count=1 per thread; setup {setup:.1f}s, "
-                                   f"run {run_s:.1f}s)"},
+                         "sample": f"all {ENVS_PER_GPU} envs x 1000 agents over {threads} threads "
+                                   f"(one reference world with StepEngine worker_count=1 per thread), "
+                                   f"{args.steps} steps after {args.warmup} warm-up; setup {setup:.1f}s, "
+                                   f"run {run_s:.1f}s"},
         "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -166,21 +204,48 @@ def run_reference(args, rank, world):
 
 
 # ---- our arm ---------------------------------------------------------------------
+def reference_engine_sample(threads, envs=256, steps=20, timeout=180):
+    """CPU variant (i), reference-faithful: ONE reference world whose
+    StepEngine runs worker_count = host threads (step_engine.cpp:17-33),
+    RolloutDriver::step with zero logits, as measure_rollout_sps
+    (harness.cpp:715-741) — in a child process under a watchdog, because the
+    engine's phase barrier can race and hang at workers > 1."""
+    code = ("import json, oracle as O; c = O.make_config(**%r); "
+            "print(json.dumps(O.bench_reference_engine(c, %d, %d, 3, %d)))" % (C2, envs, threads, steps))
+    t0 = time.perf_counter()
+    try:
+        out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                             timeout=timeout)
+        sps, setup, run_s = json.loads(out.stdout.strip().splitlines()[-1])
+        return {"value": sps, "unit": "env-steps/s", "cores": threads, "kind": "reference",
+                "sample": f"one world of {envs} envs x 1000 agents, StepEngine worker_count={threads}, "
+                          f"{steps} steps after 3 warm-up (setup {setup:.1f}s, run {run_s:.2f}s)"}
+    except subprocess.TimeoutExpired:
+        return {"value": None, "unit": "env-steps/s", "cores": threads, "kind": "reference",
+                "sample": f"HUNG: no result within the {timeout}s watchdog (engine race, SURVEY.md §5)"}
+    except Exception as e:
+        return {"value": None, "unit": "env-steps/s", "cores": threads, "kind": "reference",
+                "sample": f"failed after {time.perf_counter() - t0:.1f}s: {e}"}
+
+
 def cpu_baseline_sample(args):
-    """The reference (oracle/_ref) timed on this box's host cores on a bounded
-    sample of C2 (rank 0, N=1 only)."""
+    """The reference (oracle/_ref) timed on this box's host cores (rank 0, N=1
+    only): (ii) sharded over all 2000 envs — the headline baseline — and (i)
+    the reference-faithful multi-worker engine on a bounded sample."""
     try:
         import oracle as O
         if not O.ref_available():
             return None
-        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        threads = host_threads()
         cfg = O.make_config(**C2)
-        sps, setup, run_s = O.bench_reference_sharded(cfg, args.ref_envs_per_thread, threads, 3,
-                                                      args.cpu_steps)
-        return {"value": sps, "unit": "env-steps/s", "cores": threads, "kind": "reference",
-                "sample": f"{threads} threads x {args.ref_envs_per_thread} envs x 1000 agents x "
-                          f"{args.cpu_steps} steps (reference sources compiled in oracle/_ref, "
-                          f"StepEngine worker_count=1 per shard; run {run_s:.1f}s)"}
+        sps, setup, run_s = O.bench_reference_total(cfg, ENVS_PER_GPU, threads, 3, args.cpu_steps)
+        out = {"value": sps, "unit": "env-steps/s", "cores": threads, "kind": "reference",
+               "sample": f"all {ENVS_PER_GPU} envs x 1000 agents x {args.cpu_steps} steps over {threads} "
+                         f"threads (reference sources compiled in oracle/_ref, one StepEngine "
+                         f"worker_count=1 world per thread; setup {setup:.1f}s, run {run_s:.1f}s)"}
+        if not args.no_engine_baseline:
+            out["reference_engine"] = reference_engine_sample(threads)
+        return out
     except Exception as e:  # baseline is reported, never required
         return {"value": None, "unit": "env-steps/s", "cores": 0, "kind": "reference",
                 "sample": f"failed: {e}"}
@@ -203,19 +268,42 @@ def run_ours(args, rank, world, local_rank):
     geo = ws.plan.geometry()
     stats_t = torch.zeros(8, dtype=torch.float64, device="cuda")
 
+    # The statistics all-reduce (the path's only collective): through the
+    # library's NCCL entry point (wdg_stats_allreduce) on the store's stream.
+    # The test-only --same-device mode (all ranks on cuda:0, where NCCL cannot
+    # run two ranks) reduces on device and sums the 8 doubles over gloo.
+    comm = None
+    collective = None
+    if world > 1:
+        if args.same_device:
+            collective = {"backend": "gloo (same-device test mode)"}
+        else:
+            uid = [W.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = W.Comm(world, rank, uid[0])
+            collective = {"backend": "nccl", "nccl_version": W.nccl_version(), "comm_world": comm.world,
+                          "entry": "wdg_stats_allreduce (tracker reduce + ncclAllReduce sum, 8 doubles)"}
+
     def barrier():
         if world > 1:
             dist.barrier()
 
     def stats_allreduce():
-        drv.reduce_stats_into(stats_t)
-        if world > 1:
-            dist.all_reduce(stats_t)
+        if comm is not None:
+            comm.stats_allreduce(drv, stats_t)
+        else:
+            drv.reduce_stats_into(stats_t)
+            if world > 1:
+                host = stats_t.cpu()
+                dist.all_reduce(host)
+                stats_t.copy_(host)
 
     clocks = ClockSampler(local_rank).start()
     # ---- device-resident timed region ----
     for _ in range(args.warmup):
         drv.step()
+    if world > 1:
+        stats_allreduce()  # communicator warm-up
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -224,15 +312,20 @@ def run_ours(args, rank, world, local_rank):
     ev0.record(stream)
     launches0 = drv.launches()
     stats_launches = 0
+    allreduces = 0
+    # At least one all-reduce inside every timed window, plus one at its end.
+    stats_every = max(1, min(args.stats_every, args.steps))
     # One fused launch per step (RolloutDriver::step): each step's 328 MB
     # working set (80 MB logits read + state + 184 MB observations written)
     # exceeds the 126 MB L2, so no step finds the previous step's inputs there.
     for i in range(args.steps):
         drv.step()
-        if world > 1 and (i + 1) % args.stats_every == 0:
+        if world > 1 and ((i + 1) % stats_every == 0 or i + 1 == args.steps):
             stats_allreduce()
-            stats_launches += 2  # tracker reduce + NCCL all-reduce
+            stats_launches += 2  # tracker reduce + all-reduce
+            allreduces += 1
     ev1.record(stream)
+    clocks.sample_now()  # the GPU is still working through the enqueued window
     launches = drv.launches() - launches0 + stats_launches
     torch.cuda.synchronize()
     clocks.active = False
@@ -260,11 +353,14 @@ def run_ours(args, rank, world, local_rank):
         drv.step()
     torch.cuda.synchronize()
     es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.active = True
     es0.record(stream)
     for _ in range(stress_steps):
         drv.step()
     es1.record(stream)
+    clocks.sample_now()
     torch.cuda.synchronize()
+    clocks.active = False
     stress_ms = es0.elapsed_time(es1)
     drv.set_logits(None, 0)
     drv.check()
@@ -318,24 +414,47 @@ def run_ours(args, rank, world, local_rank):
     host_logits = torch.zeros(n_logits, dtype=torch.float64).pin_memory()
     host_rewards = torch.empty(E * A, dtype=torch.float32).pin_memory()
     host_done = torch.empty(E, dtype=torch.uint8).pin_memory()
+    host_obs = torch.empty(E * A * D, dtype=torch.float32).pin_memory()
+    done_np = host_done.numpy()
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    for _ in range(min(args.warmup, 5)):
-        drv.step_host(host_logits, n_logits, host_rewards, host_done)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    clocks.active = True
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        drv.step_host(host_logits, n_logits, host_rewards, host_done)
-    ws.store.synchronize()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    clocks.active = False
-    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * E * e2e_steps / float(te.item())
+
+    def e2e_leg(with_obs, closed):
+        obs, n_obs = (host_obs, E * A * D) if with_obs else (None, 0)
+        for _ in range(min(args.warmup, 5)):
+            drv.step_host(host_logits, n_logits, host_rewards, host_done, obs, n_obs)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clocks.active = True
+        dones = 0
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            drv.step_host(host_logits, n_logits, host_rewards, host_done, obs, n_obs)
+            if closed:  # the learner waits for step t's outputs before computing t+1's logits
+                ws.store.synchronize()
+                dones += int(done_np.sum())
+        ws.store.synchronize()
+        clocks.sample_now()
+        e2e_s = time.perf_counter() - t0
+        clocks.active = False
+        te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        v = world * E * e2e_steps / float(te.item())
+        d2h = E * A * 4 + E + (E * A * D * 4 if with_obs else 0)
+        return {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": n_logits * 8,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "pcie_gbs": (v / world) / E * (n_logits * 8 + d2h) / 1e9,
+                "closed_loop": closed, "episode_ends_seen": dones if closed else None}
+
+    e2e = e2e_leg(False, True)
+    e2e["path"] = ("wdg_rollout_step_host, closed loop: pinned host logits -> fused kernel (pipelined over "
+                   "env chunks) -> rewards + done before reset-on-done -> host waits and reads them")
+    e2e_obs = e2e_leg(True, True)
+    e2e_obs["path"] = "wdg_rollout_step_host_obs, closed loop, + post-reset observations to the host"
+    e2e_open = e2e_leg(False, False)
+    e2e_open["path"] = "wdg_rollout_step_host, open loop (no host wait between steps)"
+    drv.check()
     clocks.stop()
 
     if rank == 0:
@@ -357,15 +476,15 @@ def run_ours(args, rank, world, local_rank):
                        "kernel_geometry": geo},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": "profile-derived: dram__bytes_read.sum + dram__bytes_write.sum of "
+                                           "one ncu --set full capture of this kernel at C2 "
+                                           "(profiles/ncu_traffic.json), not measured in this run",
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_env_step": b_env,
                          "kernel": "tag_env_kernel<discrete,partial,grid> (fused step)"},
-            "e2e": {"value": e2e_value, "unit": "env-steps/s",
-                    "h2d_bytes_per_step": n_logits * 8, "d2h_bytes_per_step": E * A * 4 + E,
-                    # per-rank PCIe upload rate implied by the e2e value (bound: the link's
-                    # pinned H2D rate, 55.3 GB/s measured by tools/h2d_probe.py)
-                    "h2d_gbs": (e2e_value / world) / E * n_logits * 8 / 1e9,
-                    "path": "wdg_rollout_step_host (pinned host logits -> fused kernel -> rewards+done)"},
+            "e2e": e2e,
+            "e2e_with_obs": e2e_obs,
+            "e2e_open_loop": e2e_open,
             "sampler_stress": {"logits": "N(0, 3^2), seed 1234", "steps": stress_steps,
                                "env_steps_per_s": E * stress_steps / (stress_ms / 1e3),
                                "ms_per_step": stress_ms / stress_steps},
@@ -376,9 +495,15 @@ def run_ours(args, rank, world, local_rank):
             "episode_stats": {"episodes": stats[0], "tag_events": stats[3], "env_steps": stats[4]},
             "clocks": clocks.summary(),
         }
+        if world > 1:
+            collective["allreduces_timed"] = allreduces
+            collective["stats_every"] = stats_every
+            line["collective"] = collective
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample(args)
         print(json.dumps(line))
+    if comm is not None:
+        comm.close()
     ws.close()
     return 0
 
@@ -391,10 +516,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--stats-every", type=int, default=100)
     ap.add_argument("--e2e-steps", type=int, default=200)
-    ap.add_argument("--cpu-steps", type=int, default=12000)  # ~10 s of reference CPU work at C2
-    ap.add_argument("--ref-envs-per-thread", type=int, default=4)
-    ap.add_argument("--ref-inner", type=int, default=1)
+    ap.add_argument("--cpu-steps", type=int, default=400)  # ~10 s of reference CPU work over 2000 envs
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-engine-baseline", action="store_true")
     # Test-only: run every rank on cuda:0 over gloo, to exercise the N>1
     # logic (shards, barriers, max-over-ranks, stats all-reduce) on one GPU.
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
@@ -413,6 +537,9 @@ def main():
         if args.same_device:
             dist.init_process_group("gloo")
         else:
+            # communicator size / transport (NVLS, P2P) in the log (stderr)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         return run_ours(args, rank, world, local_rank)

@@ -292,6 +292,29 @@ WDG_API wdg_status wdg_rollout_stats_device_ptr(wdg_rollout* rollout, double** o
  * store's stream (e.g. a tensor that is then all-reduced over NCCL). */
 WDG_API wdg_status wdg_rollout_reduce_stats_into(wdg_rollout* rollout, double* device_out);
 
+/* ---- Multi-GPU: the episode-statistics all-reduce ------
+ * Envs shard across GPUs as contiguous blocks with global env ids
+ * (wdg_store_set_env_offset); the only collective is the all-reduce of the
+ * EpisodeTracker sums (trainer.cpp:221-258), exact for integer-valued
+ * rewards. libnccl.so.2 is resolved at run time (the copy already loaded in
+ * the process, e.g. PyTorch's, else the system one). */
+typedef struct wdg_comm wdg_comm;
+WDG_API wdg_status wdg_nccl_version(int32_t* out);
+/* ncclGetUniqueId into a 128-byte buffer (rank 0; share it with the others). */
+WDG_API wdg_status wdg_comm_unique_id(uint8_t* out, int64_t bytes);
+/* ncclCommInitRank: collective over all `world` ranks, one GPU each (the
+ * caller's current device). */
+WDG_API wdg_status wdg_comm_init(int32_t world, int32_t rank, const uint8_t* id, int64_t bytes,
+                                 wdg_comm** out);
+/* Wrap an existing ncclComm_t (not destroyed by wdg_comm_destroy). */
+WDG_API wdg_status wdg_comm_wrap(void* nccl_comm, wdg_comm** out);
+WDG_API void wdg_comm_destroy(wdg_comm* comm);
+WDG_API wdg_status wdg_comm_info(const wdg_comm* comm, int32_t* world, int32_t* rank);
+/* Reduce this shard's tracker slots into device_out (device double
+ * [WDG_STAT_COUNT]) and ncclAllReduce(sum) it in place over `comm`, on the
+ * store's stream; every rank then holds the global statistics. */
+WDG_API wdg_status wdg_stats_allreduce(wdg_rollout* rollout, wdg_comm* comm, double* device_out);
+
 /* ---- Policy network (proj/include/warp/policy_model.hpp) --------------- */
 /* The rollout's forward_policies (harness.cpp:445-476) on device: the
  * reference MLP (tanh hidden layers, a linear logit head per category, a

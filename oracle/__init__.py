@@ -201,6 +201,11 @@ def ref_lib():
         lib.ref_bench_sharded.restype = C.c_int
         lib.ref_bench_sharded.argtypes = [C.POINTER(TagConfigC), C.c_int64, C.c_int, C.c_int64, C.c_int64,
                                           C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        for fn in ("ref_bench_sharded_total", "ref_bench_engine"):
+            f = getattr(lib, fn)
+            f.restype = C.c_int
+            f.argtypes = [C.POINTER(TagConfigC), C.c_int64, C.c_int, C.c_int64, C.c_int64,
+                          C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         if hasattr(lib, "ref_config_canonical"):
             lib.ref_config_canonical.restype = C.c_int64
             lib.ref_config_canonical.argtypes = [C.c_char_p, C.c_int32, C.c_char_p, C.c_int64]
@@ -370,6 +375,30 @@ def bench_reference_sharded(cfg: TagConfigC, envs_per_thread: int, threads: int,
                                C.byref(sps), C.byref(setup), C.byref(run))
     if st != 0:
         raise RuntimeError(f"ref_bench_sharded: {st} {lib.ref_last_error().decode()}")
+    return sps.value, setup.value, run.value
+
+
+def bench_reference_total(cfg: TagConfigC, total_envs: int, threads: int, warmup: int, steps: int):
+    """The reference RolloutDriver loop over `total_envs` envs split across
+    `threads` independent single-worker worlds. (env_steps_per_s, setup_s, run_s)."""
+    lib = ref_lib()
+    sps, setup, run = C.c_double(), C.c_double(), C.c_double()
+    st = lib.ref_bench_sharded_total(C.byref(cfg), total_envs, threads, warmup, steps,
+                                     C.byref(sps), C.byref(setup), C.byref(run))
+    if st != 0:
+        raise RuntimeError(f"ref_bench_sharded_total: {st} {lib.ref_last_error().decode()}")
+    return sps.value, setup.value, run.value
+
+
+def bench_reference_engine(cfg: TagConfigC, num_envs: int, workers: int, warmup: int, steps: int):
+    """ONE reference world whose StepEngine runs `workers` threads (may hang at
+    workers > 1: run it in a child process). (env_steps_per_s, setup_s, run_s)."""
+    lib = ref_lib()
+    sps, setup, run = C.c_double(), C.c_double(), C.c_double()
+    st = lib.ref_bench_engine(C.byref(cfg), num_envs, workers, warmup, steps,
+                              C.byref(sps), C.byref(setup), C.byref(run))
+    if st != 0:
+        raise RuntimeError(f"ref_bench_engine: {st} {lib.ref_last_error().decode()}")
     return sps.value, setup.value, run.value
 
 

@@ -69,7 +69,7 @@ struct World {
   int64_t C = 1, V = 5;
 };
 
-World* make_world(const warp::TagConfig& cfg, int64_t num_envs, bool sequential) {
+World* make_world(const warp::TagConfig& cfg, int64_t num_envs, bool sequential, int workers = 1) {
   auto w = std::make_unique<World>();
   w->cfg = cfg;
   cfg.validate();
@@ -90,7 +90,7 @@ World* make_world(const warp::TagConfig& cfg, int64_t num_envs, bool sequential)
     warp::EngineConfig ecfg;
     ecfg.num_envs = num_envs;
     ecfg.num_agents = cfg.num_agents();
-    ecfg.worker_count = 1;
+    ecfg.worker_count = workers;
     w->engine = std::make_unique<warp::StepEngine>(ecfg);
     policy.reinitialize = warp::make_tag_reinit(w->plan);
   }
@@ -254,32 +254,37 @@ __attribute__((visibility("default"))) int ref_hw_threads(void) {
   return n == 0 ? 1 : static_cast<int>(n);
 }
 
-// CPU baseline: `threads` independent single-worker reference worlds of
-// `envs_per_thread` envs each (the race-free sharded form of the reference's
-// StepEngine), each running RolloutDriver::step with zero
+// CPU baseline (ii): `threads` independent single-worker reference worlds
+// sharing `total_envs` envs (the race-free sharded form of the reference's
+// StepEngine; shard i holds total/threads envs, the first
+// total % threads one more), each running RolloutDriver::step with zero
 // logits. Times `steps` steps after `warmup` steps with all threads released
 // together; returns aggregate env-steps/s and the setup seconds.
-__attribute__((visibility("default"))) int ref_bench_sharded(const wdg_tag_config* cfg,
-                                                             int64_t envs_per_thread, int threads,
-                                                             int64_t warmup, int64_t steps,
-                                                             double* env_steps_per_s,
-                                                             double* setup_s, double* run_s) {
+__attribute__((visibility("default"))) int ref_bench_sharded_total(const wdg_tag_config* cfg,
+                                                                   int64_t total_envs, int threads,
+                                                                   int64_t warmup, int64_t steps,
+                                                                   double* env_steps_per_s,
+                                                                   double* setup_s, double* run_s) {
   return guarded([&] {
     using Clock = std::chrono::steady_clock;
     const warp::TagConfig tc = to_ref(*cfg);
+    threads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(threads, total_envs)));
+    std::vector<int64_t> share(static_cast<size_t>(threads), total_envs / threads);
+    for (int64_t i = 0; i < total_envs % threads; ++i) ++share[static_cast<size_t>(i)];
     std::vector<std::unique_ptr<World>> worlds(static_cast<size_t>(threads));
     const auto t0 = Clock::now();
     {
       std::vector<std::thread> pool;
       for (int i = 0; i < threads; ++i) {
-        pool.emplace_back([&, i] { worlds[static_cast<size_t>(i)].reset(make_world(tc, envs_per_thread, false)); });
+        pool.emplace_back([&, i] {
+          worlds[static_cast<size_t>(i)].reset(make_world(tc, share[static_cast<size_t>(i)], false));
+        });
       }
       for (auto& t : pool) t.join();
     }
     const auto t1 = Clock::now();
     std::atomic<int> ready{0};
     std::atomic<bool> go{false};
-    std::vector<double> secs(static_cast<size_t>(threads), 0.0);
     std::vector<std::thread> pool;
     for (int i = 0; i < threads; ++i) {
       pool.emplace_back([&, i] {
@@ -287,9 +292,7 @@ __attribute__((visibility("default"))) int ref_bench_sharded(const wdg_tag_confi
         for (int64_t s = 0; s < warmup; ++s) step_world(w, nullptr, s, tc.seed);
         ready.fetch_add(1);
         while (!go.load()) std::this_thread::yield();
-        const auto a = Clock::now();
         for (int64_t s = 0; s < steps; ++s) step_world(w, nullptr, warmup + s, tc.seed);
-        secs[static_cast<size_t>(i)] = std::chrono::duration<double>(Clock::now() - a).count();
       });
     }
     while (ready.load() < threads) std::this_thread::yield();
@@ -299,7 +302,43 @@ __attribute__((visibility("default"))) int ref_bench_sharded(const wdg_tag_confi
     const double wall = std::chrono::duration<double>(Clock::now() - r0).count();
     *setup_s = std::chrono::duration<double>(t1 - t0).count();
     *run_s = wall;
-    *env_steps_per_s = static_cast<double>(envs_per_thread) * threads * steps / wall;
+    *env_steps_per_s = static_cast<double>(total_envs) * steps / wall;
+    return 0;
+  });
+}
+
+__attribute__((visibility("default"))) int ref_bench_sharded(const wdg_tag_config* cfg,
+                                                             int64_t envs_per_thread, int threads,
+                                                             int64_t warmup, int64_t steps,
+                                                             double* env_steps_per_s,
+                                                             double* setup_s, double* run_s) {
+  return ref_bench_sharded_total(cfg, envs_per_thread * threads, threads, warmup, steps, env_steps_per_s,
+                                 setup_s, run_s);
+}
+
+// CPU baseline (i), reference-faithful: ONE world whose StepEngine runs
+// `workers` threads (step_engine.cpp:17-33), driven by RolloutDriver::step
+// (harness.cpp:478-490) with zero logits, as measure_rollout_sps does
+// (harness.cpp:715-741). The engine's phase barrier can race and hang at
+// workers > 1: callers run this in a child process under a
+// watchdog.
+__attribute__((visibility("default"))) int ref_bench_engine(const wdg_tag_config* cfg, int64_t num_envs,
+                                                            int workers, int64_t warmup, int64_t steps,
+                                                            double* env_steps_per_s, double* setup_s,
+                                                            double* run_s) {
+  return guarded([&] {
+    using Clock = std::chrono::steady_clock;
+    const warp::TagConfig tc = to_ref(*cfg);
+    const auto t0 = Clock::now();
+    std::unique_ptr<World> w(make_world(tc, num_envs, false, std::max(1, workers)));
+    const auto t1 = Clock::now();
+    for (int64_t s = 0; s < warmup; ++s) step_world(w.get(), nullptr, s, tc.seed);
+    const auto r0 = Clock::now();
+    for (int64_t s = 0; s < steps; ++s) step_world(w.get(), nullptr, warmup + s, tc.seed);
+    const double wall = std::chrono::duration<double>(Clock::now() - r0).count();
+    *setup_s = std::chrono::duration<double>(t1 - t0).count();
+    *run_s = wall;
+    *env_steps_per_s = static_cast<double>(num_envs) * steps / wall;
     return 0;
   });
 }

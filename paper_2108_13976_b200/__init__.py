@@ -71,7 +71,8 @@ EXPORTED_SYMBOLS = [
     "wdg_rollout_next_step", "wdg_rollout_check", "wdg_rollout_stats", "wdg_rollout_reset_stats",
     "wdg_rollout_stats_device_ptr", "wdg_rollout_step_host", "wdg_rollout_step_host_obs",
     "wdg_rollout_set_host_chunks", "wdg_rollout_reduce_stats_into", "wdg_rollout_set_overlap",
-    "wdg_set_tuning",
+    "wdg_set_tuning", "wdg_nccl_version", "wdg_comm_unique_id", "wdg_comm_init", "wdg_comm_wrap",
+    "wdg_comm_destroy", "wdg_comm_info", "wdg_stats_allreduce",
     "wdg_policy_create", "wdg_policy_destroy", "wdg_policy_init", "wdg_policy_param_count",
     "wdg_policy_set_params", "wdg_policy_get_params", "wdg_policy_forward", "wdg_rollout_set_policies",
     "wdg_rollout_policy_outputs", "wdg_copy_to_host", "wdg_rollout_set_keep_policy_outputs",
@@ -194,6 +195,13 @@ def _load():
         "wdg_rollout_set_host_chunks": (I32, [P, I32]),
         "wdg_rollout_set_overlap": (I32, [P, I32]),
         "wdg_set_tuning": (I32, [C.c_char_p, I64]),
+        "wdg_nccl_version": (I32, [C.POINTER(I32)]),
+        "wdg_comm_unique_id": (I32, [P, I64]),
+        "wdg_comm_init": (I32, [I32, I32, P, I64, C.POINTER(P)]),
+        "wdg_comm_wrap": (I32, [P, C.POINTER(P)]),
+        "wdg_comm_destroy": (None, [P]),
+        "wdg_comm_info": (I32, [P, C.POINTER(I32), C.POINTER(I32)]),
+        "wdg_stats_allreduce": (I32, [P, P, P]),
         "wdg_rollout_reduce_stats_into": (I32, [P, P]),
         "wdg_policy_create": (I32, [I64, C.POINTER(I64), I32, I64, I64, C.POINTER(P)]),
         "wdg_policy_destroy": (None, [P]),
@@ -727,6 +735,54 @@ class RolloutDriver:
         p = C.POINTER(C.c_double)()
         _check(self._lib.wdg_rollout_stats_device_ptr(self._h, C.byref(p)))
         return C.cast(p, C.c_void_p).value or 0
+
+
+def nccl_version() -> int:
+    v = C.c_int32()
+    _check(_load().wdg_nccl_version(C.byref(v)))
+    return v.value
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 creates it, every rank passes it to Comm)."""
+    buf = (C.c_uint8 * 128)()
+    _check(_load().wdg_comm_unique_id(buf, 128))
+    return bytes(buf)
+
+
+class Comm:
+    """NCCL communicator of the statistics all-reduce (wdg_comm_*): created
+    from a unique id (ncclCommInitRank over `world` ranks, one GPU each), or
+    wrapping an existing ncclComm_t address (e.g. ProcessGroupNCCL._comm_ptr())."""
+
+    def __init__(self, world: int = 1, rank: int = 0, unique_id: Optional[bytes] = None,
+                 wrap: Optional[int] = None):
+        self._lib = _load()
+        h = C.c_void_p()
+        if wrap is not None:
+            _check(self._lib.wdg_comm_wrap(C.c_void_p(wrap), C.byref(h)))
+        else:
+            if unique_id is None or len(unique_id) != 128:
+                raise ValueError("Comm needs the 128-byte unique id from comm_unique_id()")
+            buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+            _check(self._lib.wdg_comm_init(world, rank, buf, 128, C.byref(h)))
+        self._h = h
+        w, r = C.c_int32(), C.c_int32()
+        _check(self._lib.wdg_comm_info(h, C.byref(w), C.byref(r)))
+        self.world, self.rank = w.value, r.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wdg_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def stats_allreduce(self, rollout: "RolloutDriver", device_out):
+        """This shard's tracker sums reduced on device, then ncclAllReduce(sum)
+        into device_out (device double[8]) on the store's stream."""
+        _check(self._lib.wdg_stats_allreduce(rollout._h, self._h, C.c_void_p(_ptr(device_out))))
 
 
 class Policy:

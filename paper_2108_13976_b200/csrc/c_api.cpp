@@ -30,6 +30,10 @@ struct wdg_policy {
 struct wdg_batch {
   std::unique_ptr<wdg::RolloutBatch> impl;
 };
+struct wdg_comm {
+  wdg::Comm* impl = nullptr;
+  ~wdg_comm() { wdg::comm_destroy(impl); }
+};
 struct wdg_session {
   wdg::Session* impl = nullptr;
   ~wdg_session() { wdg::session_close(impl); }
@@ -418,6 +422,50 @@ wdg_status wdg_rollout_set_host_chunks(wdg_rollout* r, int32_t chunks) {
 
 wdg_status wdg_rollout_reduce_stats_into(wdg_rollout* r, double* device_out) {
   return guarded([&] { need(r, "rollout")->impl->reduce_stats_into(device_out); });
+}
+
+// ---- NCCL statistics all-reduce -------------------------
+wdg_status wdg_nccl_version(int32_t* out) {
+  return guarded([&] { *need(out, "out") = wdg::comm_nccl_version(); });
+}
+
+wdg_status wdg_comm_unique_id(uint8_t* out, int64_t bytes) {
+  return guarded([&] { wdg::comm_unique_id(out, bytes); });
+}
+
+wdg_status wdg_comm_init(int32_t world, int32_t rank, const uint8_t* id, int64_t bytes, wdg_comm** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto c = std::make_unique<wdg_comm>();
+    c->impl = wdg::comm_init(world, rank, id, bytes);
+    *out = c.release();
+  });
+}
+
+wdg_status wdg_comm_wrap(void* nccl_comm, wdg_comm** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto c = std::make_unique<wdg_comm>();
+    c->impl = wdg::comm_wrap(nccl_comm);
+    *out = c.release();
+  });
+}
+
+void wdg_comm_destroy(wdg_comm* comm) { delete comm; }
+
+wdg_status wdg_comm_info(const wdg_comm* comm, int32_t* world, int32_t* rank) {
+  return guarded([&] {
+    const wdg::Comm* c = need(need(comm, "comm")->impl, "comm");
+    if (world) *world = c->world;
+    if (rank) *rank = c->rank;
+  });
+}
+
+wdg_status wdg_stats_allreduce(wdg_rollout* r, wdg_comm* comm, double* device_out) {
+  return guarded([&] {
+    if (device_out == nullptr) wdg::raise(wdg::Errc::invalid_argument, "stats_allreduce: null output");
+    wdg::stats_allreduce(*need(r, "rollout")->impl, need(need(comm, "comm")->impl, "comm"), device_out);
+  });
 }
 
 wdg_status wdg_rollout_run(wdg_rollout* r, int64_t steps) {

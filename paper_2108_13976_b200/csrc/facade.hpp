@@ -261,6 +261,7 @@ class Rollout {
   void run(int64_t steps);
   void reduce_stats_into(double* device_out);
   int64_t next_step() const { return t_; }
+  cudaStream_t stream() const { return store_.stream(); }
   // Kernel launches this driver has issued (env step kernels, policy
   // forwards, graph replays counted per node).
   int64_t launches() const { return launches_; }
@@ -351,6 +352,20 @@ inline constexpr uint64_t kStreamActions = 0x616374696f6e7331ULL;
 inline constexpr uint64_t kStreamPlacement = 0x706c6163656d656eULL;
 
 float& fault_tag_radius_bias();
+// NCCL communicator for the episode-statistics all-reduce (comm.cpp).
+struct Comm {
+  void* nccl;   // ncclComm_t
+  bool owned;   // created here (destroyed here) or wrapped
+  int32_t world, rank;
+};
+int32_t comm_nccl_version();
+void comm_unique_id(uint8_t* out, int64_t bytes);
+Comm* comm_init(int32_t world, int32_t rank, const uint8_t* id, int64_t bytes);
+Comm* comm_wrap(void* nccl_comm);
+void comm_destroy(Comm* c);
+void comm_allreduce_sum_f64(Comm* c, double* buf, int64_t count, cudaStream_t st);
+void stats_allreduce(Rollout& r, Comm* c, double* device_out);
+
 // Plan tuning overrides (tag.cpp kTuningKeys); "reset" restores the defaults.
 void set_tuning(const std::string& key, int64_t value);
 
