@@ -188,6 +188,15 @@ typedef struct wdg_tag_plan wdg_tag_plan;
  * the store (same ownership rule as TagContext, tag_env.cpp:351-361). */
 WDG_API wdg_status wdg_build_tag_plan(wdg_store* store, const wdg_tag_config* cfg,
                                       wdg_tag_plan** out);
+/* TagReference(store, cfg) (tag_env.cpp:505-595) on device: a plan whose
+ * run_step and reset reinit run an independent brute-force twin of the step
+ * (global memory only, brute-force K-NN and resolve, any K < A) instead of
+ * the production kernel — the second store of the consistency check
+ * (harness.cpp:562-633). It recomputes the store's episode-0 observations
+ * itself. Not usable with the fused rollout (RolloutDriver falls back to the
+ * unfused sample -> run_step -> auto_reset sequence). */
+WDG_API wdg_status wdg_build_tag_reference(wdg_store* store, const wdg_tag_config* cfg,
+                                           wdg_tag_plan** out);
 WDG_API void wdg_tag_plan_destroy(wdg_tag_plan* plan);
 /* StepEngine::run_step(plan, store, step) (step_engine.cpp:122-138) for the
  * Tag plan: move -> resolve_tags -> observe_reward, one CTA per env. */

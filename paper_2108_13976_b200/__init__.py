@@ -71,7 +71,7 @@ EXPORTED_SYMBOLS = [
     "wdg_rollout_next_step", "wdg_rollout_check", "wdg_rollout_stats", "wdg_rollout_reset_stats",
     "wdg_rollout_stats_device_ptr", "wdg_rollout_step_host", "wdg_rollout_step_host_obs",
     "wdg_rollout_set_host_chunks", "wdg_rollout_reduce_stats_into", "wdg_rollout_set_overlap",
-    "wdg_set_tuning", "wdg_nccl_version", "wdg_comm_unique_id", "wdg_comm_init", "wdg_comm_wrap",
+    "wdg_set_tuning", "wdg_build_tag_reference", "wdg_nccl_version", "wdg_comm_unique_id", "wdg_comm_init", "wdg_comm_wrap",
     "wdg_comm_destroy", "wdg_comm_info", "wdg_stats_allreduce",
     "wdg_policy_create", "wdg_policy_destroy", "wdg_policy_init", "wdg_policy_param_count",
     "wdg_policy_set_params", "wdg_policy_get_params", "wdg_policy_forward", "wdg_rollout_set_policies",
@@ -195,6 +195,7 @@ def _load():
         "wdg_rollout_set_host_chunks": (I32, [P, I32]),
         "wdg_rollout_set_overlap": (I32, [P, I32]),
         "wdg_set_tuning": (I32, [C.c_char_p, I64]),
+        "wdg_build_tag_reference": (I32, [P, P, C.POINTER(P)]),
         "wdg_nccl_version": (I32, [C.POINTER(I32)]),
         "wdg_comm_unique_id": (I32, [P, I64]),
         "wdg_comm_init": (I32, [I32, I32, P, I64, C.POINTER(P)]),
@@ -502,10 +503,14 @@ def tag_zero_on_reset():
 class TagPlan:
     """TagPlan (tag_env.hpp:104-107); must not outlive its store."""
 
-    def __init__(self, store: DataStore, cfg: TagConfig):
+    def __init__(self, store: DataStore, cfg: TagConfig, reference: bool = False):
+        """reference=True: the device TagReference twin (tag_env.cpp:505-595),
+        the consistency check's independent brute-force implementation."""
         self._lib = _load()
         h = C.c_void_p()
-        _check(self._lib.wdg_build_tag_plan(store._h, C.byref(cfg._c()), C.byref(h)))
+        build = self._lib.wdg_build_tag_reference if reference else self._lib.wdg_build_tag_plan
+        _check(build(store._h, C.byref(cfg._c()), C.byref(h)))
+        self.reference = reference
         self._h = h
         self.store = store
         self.cfg = cfg
@@ -948,7 +953,10 @@ class Session:
 class Workspace:
     """build_workspace (harness.cpp:402-423): store + plan + engine + resets."""
 
-    def __init__(self, cfg: TagConfig, num_envs: int, env_offset: int = 0, stream=None):
+    def __init__(self, cfg: TagConfig, num_envs: int, env_offset: int = 0, stream=None,
+                 reference: bool = False):
+        """reference=True builds the device TagReference twin as the plan
+        (the check's second store, harness.cpp:572-584)."""
         cfg.validate()
         self.cfg = cfg
         self.store = DataStore(num_envs, cfg.num_agents())
@@ -958,7 +966,7 @@ class Workspace:
             self.store.set_env_offset(env_offset)
         register_tag_arrays(self.store, cfg)
         self.store.lock()
-        self.plan = build_tag_plan(self.store, cfg)
+        self.plan = TagPlan(self.store, cfg, reference=reference)
         self.engine = StepEngine(EngineConfig(num_envs, cfg.num_agents()))
         self.resets = ResetManager(self.store, ResetPolicy(True, tag_zero_on_reset(),
                                                            make_tag_reinit(self.plan)))

@@ -282,6 +282,15 @@ wdg_status wdg_build_tag_plan(wdg_store* store, const wdg_tag_config* cfg, wdg_t
   });
 }
 
+wdg_status wdg_build_tag_reference(wdg_store* store, const wdg_tag_config* cfg, wdg_tag_plan** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto p = std::make_unique<wdg_tag_plan>();
+    p->impl = std::make_unique<wdg::TagPlan>(*need(store, "store")->impl, *need(cfg, "cfg"), true);
+    *out = p.release();
+  });
+}
+
 void wdg_tag_plan_destroy(wdg_tag_plan* plan) { delete plan; }
 
 wdg_status wdg_run_step(wdg_tag_plan* plan, int64_t step_index) {

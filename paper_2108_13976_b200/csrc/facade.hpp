@@ -167,7 +167,15 @@ void register_tag_arrays(DataStore& store, const wdg_tag_config& cfg);
 // TagPlan (tag_env.hpp:104-116) + StepEngine::run_step for it.
 class TagPlan {
  public:
-  TagPlan(DataStore& store, const wdg_tag_config& cfg);
+  // reference = true: the device TagReference (twin_kernels.cu,
+  // tag_env.cpp:505-595) — run_step and reinit_masked run the independent
+  // brute-force twin instead of the production kernel (the consistency
+  // check's second store, harness.cpp:562-633).
+  TagPlan(DataStore& store, const wdg_tag_config& cfg, bool reference = false);
+  ~TagPlan();
+  TagPlan(const TagPlan&) = delete;
+  TagPlan& operator=(const TagPlan&) = delete;
+  bool reference() const { return reference_; }
   void run_step(int64_t step_index);
   void reinit_masked(const uint8_t* env_mask, int32_t* episode);
   void launch(TagLaunch L);
@@ -189,6 +197,9 @@ class TagPlan {
   TagDevConfig dev_;
   TagDevArrays arrays_;
   int multistep_ = -1;
+  bool reference_ = false;
+  float* knn_d2_ = nullptr;     // twin K-NN scratch [E*A*K]
+  int32_t* knn_idx_ = nullptr;
 };
 
 // sample_actions (sampler.hpp:35-36) with device logits.

@@ -26,6 +26,10 @@ cudaError_t launch_restore_zero(const ResetRowDesc* descs, int ndesc, const uint
                                 uint8_t* done, int32_t* episode, int64_t E, cudaStream_t st);
 // ptr[0] = value; ptr[1] = value2 when value2 >= 0
 cudaError_t launch_set_counter(int64_t* ptr, int64_t value, cudaStream_t st, int64_t value2 = -1);
+// The device TagReference (twin_kernels.cu): mode kModeStep or kModeReinit.
+cudaError_t launch_twin_kernel(const TagDevConfig& p, const TagDevArrays& g, int32_t mode,
+                               const uint8_t* env_mask, const int32_t* episode, float* knn_d2,
+                               int32_t* knn_idx, cudaStream_t st);
 cudaError_t launch_stats_reduce(const double* env_stats, int64_t E, double* out, cudaStream_t st);
 
 }  // namespace wdg

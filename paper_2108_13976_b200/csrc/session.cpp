@@ -351,14 +351,20 @@ struct World {
   std::unique_ptr<TagPlan> plan;
   std::unique_ptr<ResetManager> resets;
   std::unique_ptr<Rollout> rollout;
-  World(const wdg_tag_config& cfg, int64_t envs, uint64_t sample_seed) {
+  // reference: the plan is the device TagReference twin (twin_kernels.cu).
+  // rollout_resets = false: the rollout only samples and steps; the caller
+  // compares the stores and then runs resets->auto_reset_on_done() itself
+  // (the checker's order, harness.cpp:619-629).
+  World(const wdg_tag_config& cfg, int64_t envs, uint64_t sample_seed, bool reference = false,
+        bool rollout_resets = true) {
     validate_tag_config(cfg);
     store = std::make_unique<DataStore>(envs, cfg.num_taggers + cfg.num_runners);
     register_tag_arrays(*store, cfg);
     store->lock();
-    plan = std::make_unique<TagPlan>(*store, cfg);
+    plan = std::make_unique<TagPlan>(*store, cfg, reference);
     resets = std::make_unique<ResetManager>(*store, true, tag_zero_on_reset(), plan.get());
-    rollout = std::make_unique<Rollout>(*store, *plan, resets.get(), sample_seed);
+    rollout = std::make_unique<Rollout>(*store, *plan, rollout_resets ? resets.get() : nullptr, sample_seed);
+    if (!rollout_resets) rollout->set_fused(false);
   }
 };
 
@@ -433,6 +439,18 @@ struct Session {
   // run_step -> detect/auto_reset, separate kernels) step in lockstep with
   // the same f64 policy (init_policy(trainer.seed)); stores are compared on
   // device after every step in the reference's causal order.
+  // check (check_consistency_single, harness.cpp:562-633), per variant x
+  // obs mode, two legs with the same f64 policy init_policy(trainer.seed):
+  //  1. reference: the production plan against the device TagReference twin
+  //     (an independent brute-force implementation, twin_kernels.cu), each
+  //     step sampled from the policy forward of its own store's obs, compared
+  //     after the step and BEFORE reset-on-done in the reference's causal
+  //     order (sampled_actions, rewards, done, observations), then both reset
+  //     — exactly the reference's engine-vs-TagReference flow;
+  //  2. fused: the one-kernel RolloutDriver::step against the unfused kernel
+  //     sequence (sample -> run_step -> detect/auto_reset), compared after
+  //     every step (post-reset).
+  // A combo passes when both legs do; the row reports the first divergence.
   bool run_check() {
     validate(config);
     json j;
@@ -441,7 +459,7 @@ struct Session {
     Table t;
     meta_into(j["meta"], t);
     t.columns = {"variant", "obs_mode", "workers", "steps", "passed", "div_step", "div_array", "div_env",
-                 "div_agent", "div_index"};
+                 "div_agent", "div_index", "div_leg"};
     std::ostringstream sum;
     bool all = true;
     int n_pass = 0, n = 0;
@@ -456,9 +474,6 @@ struct Session {
         validate_tag_config(env);
         const auto t0 = Clock::now();
         const uint64_t seed = config.trainer.seed;
-        auto fused = std::make_unique<World>(env, config.engine.num_envs, seed);
-        World unfused(env, config.engine.num_envs, seed);
-        unfused.rollout->set_fused(false);
         PolicyDims dims;
         dims.obs_dim = tag_obs_dim(env);
         dims.hidden = config.trainer.hidden_sizes;
@@ -466,37 +481,71 @@ struct Session {
         dims.num_choices = variant == WDG_TAG_CONTINUOUS ? 3 : 5;
         Policy policy(dims);
         policy.init(config.trainer.seed);
-        fused->rollout->set_policies(&policy, &policy, kPolicyF64);
-        unfused.rollout->set_policies(&policy, &policy, kPolicyF64);
-        std::optional<Divergence> div;
-        for (int64_t s = 0; s < config.run.check_steps && !div; ++s) {
-          fused->rollout->step();
-          unfused.rollout->step();
-          div = compare_stores(*fused->store, *unfused.store, s, dfirst);
+        const int64_t E = config.engine.num_envs;
+        // leg 1: production plan vs the device TagReference twin
+        std::optional<Divergence> div_ref;
+        {
+          World engine(env, E, seed, false, false);
+          World twin(env, E, seed, true, false);
+          engine.rollout->set_policies(&policy, &policy, kPolicyF64);
+          twin.rollout->set_policies(&policy, &policy, kPolicyF64);
+          div_ref = compare_stores(*engine.store, *twin.store, -1, dfirst);  // registration
+          for (int64_t s = 0; s < config.run.check_steps && !div_ref; ++s) {
+            engine.rollout->step();  // forward -> sample -> run_step (no reset)
+            twin.rollout->step();
+            div_ref = compare_stores(*engine.store, *twin.store, s, dfirst);
+            engine.resets->auto_reset_on_done();
+            twin.resets->auto_reset_on_done();
+          }
+          engine.rollout->check();
+          twin.rollout->check();
         }
-        fused->rollout->check();
-        unfused.rollout->check();
+        // leg 2: fused vs unfused rollout
+        auto fused = std::make_unique<World>(env, E, seed);
+        std::optional<Divergence> div_fused;
+        {
+          World unfused(env, E, seed);
+          unfused.rollout->set_fused(false);
+          fused->rollout->set_policies(&policy, &policy, kPolicyF64);
+          unfused.rollout->set_policies(&policy, &policy, kPolicyF64);
+          for (int64_t s = 0; s < config.run.check_steps && !div_fused; ++s) {
+            fused->rollout->step();
+            unfused.rollout->step();
+            div_fused = compare_stores(*fused->store, *unfused.store, s, dfirst);
+          }
+          fused->rollout->check();
+          unfused.rollout->check();
+        }
         const double wall_ms = seconds_since(t0) * 1e3;
-        const bool passed = !div.has_value();
+        const bool passed = !div_ref && !div_fused;
+        const std::optional<Divergence>& div = div_ref ? div_ref : div_fused;
+        const char* leg = div_ref ? "reference" : (div_fused ? "fused" : "");
         all = all && passed;
         n_pass += passed ? 1 : 0;
         ++n;
         json jc = {{"variant", variant_name(variant)}, {"obs_mode", obs_name(obs)}, {"workers", 1},
                    {"steps", config.run.check_steps}, {"passed", passed}, {"wall_ms", wall_ms}};
+        auto leg_json = [](const std::optional<Divergence>& d) {
+          json l = {{"passed", !d.has_value()}};
+          if (d) l["divergence"] = {{"step", d->step}, {"array", d->array}, {"env", d->env}, {"agent", d->agent},
+                                    {"index", d->index}};
+          return l;
+        };
+        jc["legs"] = {{"reference", leg_json(div_ref)}, {"fused", leg_json(div_fused)}};
         const Divergence d = div.value_or(Divergence{});
         if (div) {
           jc["divergence"] = {{"step", d.step}, {"array", d.array}, {"env", d.env}, {"agent", d.agent},
-                              {"index", d.index}};
+                              {"index", d.index}, {"leg", leg}};
         }
         j["combos"].push_back(jc);
         t.rows.push_back({variant_name(variant), obs_name(obs), "1", std::to_string(config.run.check_steps),
                           passed ? "1" : "0", std::to_string(d.step), div ? d.array : "", std::to_string(d.env),
-                          std::to_string(d.agent), std::to_string(d.index)});
+                          std::to_string(d.agent), std::to_string(d.index), leg});
         std::ostringstream ln;
         ln << "  " << variant_name(variant) << "/" << obs_name(obs) << " workers=1 steps=" << config.run.check_steps
            << " " << (passed ? "pass" : "FAIL");
         if (div) {
-          ln << " first divergence: step=" << d.step << " array=" << d.array << " env=" << d.env
+          ln << " first divergence (" << leg << "): step=" << d.step << " array=" << d.array << " env=" << d.env
              << " agent=" << d.agent << " index=" << d.index;
         }
         lines.push_back(ln.str());

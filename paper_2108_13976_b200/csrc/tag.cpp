@@ -466,14 +466,34 @@ void register_tag_arrays(DataStore& store, const wdg_tag_config& cfg) {
 }
 
 // ---- TagPlan ---------------------------------------------------------------
-TagPlan::TagPlan(DataStore& store, const wdg_tag_config& cfg) : store_(store), cfg_(cfg) {
+TagPlan::TagPlan(DataStore& store, const wdg_tag_config& cfg, bool reference)
+    : store_(store), cfg_(cfg), reference_(reference) {
   validate_tag_config(cfg);
   if (!store.locked()) raise(Errc::state_error, "build_tag_plan: store must be locked");
   dev_ = make_dev_config(store, cfg);
   arrays_ = bind_dev_arrays(store, cfg);
+  if (reference_) {
+    if (dev_.partial) {
+      const size_t n = static_cast<size_t>(dev_.E) * dev_.A * dev_.K;
+      cuda_check(cudaMalloc(&knn_d2_, n * sizeof(float)), "cudaMalloc(twin knn)");
+      cuda_check(cudaMalloc(&knn_idx_, n * sizeof(int32_t)), "cudaMalloc(twin knn)");
+    }
+    // The episode-0 state and observations of register_tag_arrays
+    // (tag_env.cpp:288-340) recomputed by the twin itself.
+    dev_.fault_bias = 0.0f;
+    cuda_check(launch_twin_kernel(dev_, arrays_, kModeReinit, nullptr, nullptr, knn_d2_, knn_idx_,
+                                  store_.stream()),
+               "twin registration");
+  }
+}
+
+TagPlan::~TagPlan() {
+  if (knn_d2_) cudaFree(knn_d2_);
+  if (knn_idx_) cudaFree(knn_idx_);
 }
 
 void TagPlan::launch(TagLaunch L) {
+  if (reference_) raise(Errc::state_error, "tag plan: the TagReference twin runs run_step / reinit only");
   dev_.fault_bias = fault_tag_radius_bias();
   cuda_check(launch_tag_kernel(dev_, arrays_, L, store_.stream()), "tag kernel launch");
 }
@@ -532,6 +552,7 @@ bool TagPlan::multistep_ok() {
 // (global env ids) and the results equal those of a whole-store launch.
 void TagPlan::launch_envs(TagLaunch L, int64_t e0, int64_t n) {
   if (e0 == 0 && n == dev_.E) return launch(L);
+  if (reference_) raise(Errc::state_error, "tag plan: the TagReference twin runs run_step / reinit only");
   if (e0 < 0 || n <= 0 || e0 + n > dev_.E) raise(Errc::index_out_of_range, "tag launch: env range");
   TagDevConfig d = dev_;
   d.fault_bias = fault_tag_radius_bias();
@@ -571,12 +592,23 @@ void TagPlan::launch_envs(TagLaunch L, int64_t e0, int64_t n) {
 
 void TagPlan::run_step(int64_t step_index) {
   (void)step_index;  // the Tag kernels do not use the step index (tag_env.cpp:530)
+  if (reference_) {
+    cuda_check(launch_twin_kernel(dev_, arrays_, kModeStep, nullptr, nullptr, knn_d2_, knn_idx_, store_.stream()),
+               "twin step");
+    return;
+  }
   TagLaunch L;
   L.mode = kModeStep;
   launch(L);
 }
 
 void TagPlan::reinit_masked(const uint8_t* env_mask, int32_t* episode) {
+  if (reference_) {
+    cuda_check(launch_twin_kernel(dev_, arrays_, kModeReinit, env_mask, episode, knn_d2_, knn_idx_,
+                                  store_.stream()),
+               "twin reinit");
+    return;
+  }
   TagLaunch L;
   L.mode = kModeReinit;
   L.env_mask = env_mask;
@@ -811,7 +843,7 @@ void Rollout::set_logits(const double* logits, int64_t count) {
 }
 
 bool Rollout::fused_ok() const {
-  return fused_ && (resets_ == nullptr || !resets_->auto_enabled() ||
+  return fused_ && !plan_.reference() && (resets_ == nullptr || !resets_->auto_enabled() ||
                     (resets_->tag_default() && resets_->reinit_plan() == &plan_));
 }
 

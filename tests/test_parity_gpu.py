@@ -215,9 +215,10 @@ GOLDEN = sorted(f for f in os.listdir(os.path.join(HERE, "golden")) if f.endswit
 @pytest.mark.parametrize("fname", GOLDEN)
 def test_golden_fixture_on_device(fname):
     """Replays a fixture generated by the reference itself (make_golden.py):
-    discrete fixtures must reproduce the reference's per-step digests exactly;
-    continuous fixtures are replayed teacher-forced-free and must keep every
-    integer/flag array exact for the first steps and f32 within tolerance."""
+    the device must reproduce the reference's per-step digests (FNV-1a over
+    every array, after the step and after the reset) exactly — discrete and
+    continuous (the device replays the reference host's glibc sinf/cosf
+    bit-for-bit, §8f row 4) — and its final arrays and episode counters."""
     g = np.load(os.path.join(HERE, "golden", fname))
     name = fname[:-4]
     spec = MG.CONFIGS[name]
@@ -227,24 +228,20 @@ def test_golden_fixture_on_device(fname):
     names = list(O.array_layout(oc, envs).keys())
     cont = dc.variant == W.CONTINUOUS
     init = {n: g["init_" + n] for n in names}
-    assert_same(dev_snapshot(ws, names), init, "init", cont=cont)
+    assert_same(dev_snapshot(ws, names), init, "init")
     A, C, V = dc.num_agents(), dc.action_categories(), dc.action_choices()
     step_dig = json.loads(str(g["step_digest"]))
     reset_dig = json.loads(str(g["reset_digest"]))
-    steps = spec["steps"] if not cont else 5
-    for t in range(steps):
+    for t in range(spec["steps"]):
         lg = MG.logits_for(name, oc, envs, t) if spec.get("logits") else np.zeros((envs, A, C, V))
         W.sample_actions(ws.store, to_dev(lg), lg.size, C, V, t, oc.seed)
         ws.engine.run_step(ws.plan, ws.store, t)
-        if not cont:
-            assert MG.digest(dev_snapshot(ws, names)) == step_dig[t], f"step {t}"
+        assert MG.digest(dev_snapshot(ws, names)) == step_dig[t], f"{'cont ' if cont else ''}step {t}"
         ws.resets.auto_reset(ws.resets.detect_done())
-        if not cont:
-            assert MG.digest(dev_snapshot(ws, names)) == reset_dig[t], f"reset {t}"
-    if not cont:
-        final = {n: g["final_" + n] for n in names}
-        assert_same(dev_snapshot(ws, names), final, "final")
-        assert [ws.resets.episodes_started(e) for e in range(envs)] == list(g["episodes"])
+        assert MG.digest(dev_snapshot(ws, names)) == reset_dig[t], f"{'cont ' if cont else ''}reset {t}"
+    final = {n: g["final_" + n] for n in names}
+    assert_same(dev_snapshot(ws, names), final, "final")
+    assert [ws.resets.episodes_started(e) for e in range(envs)] == list(g["episodes"])
     ws.close()
 
 
@@ -445,6 +442,36 @@ def test_reset_manager_policy_validation():
     with pytest.raises(W.WarpError) as ei:
         W.ResetManager(ws.store, W.ResetPolicy(True, ["nope"], None))
     assert ei.value.code == W.UNKNOWN_NAME
+    ws.close()
+
+
+@pytest.mark.parametrize("name", ["disc_full_60x12", "disc_part_60x12", "disc_part_7x100_k7",
+                                  "disc_part_3x1000", "disc_part_9x33_k20", "disc_part_3x250_ring"]
+                         + list(CONT_CONFIGS))
+def test_device_tag_reference_twin_matches_oracle(name):
+    """The device TagReference twin (twin_kernels.cu, the check's independent
+    second implementation) against the oracle: unfused sample -> run_step ->
+    auto_reset, bit-exact on every array (continuous too: same libm replica)."""
+    kw, envs = {**CONFIGS, **CONT_CONFIGS}[name]
+    if name in CONT_CONFIGS and not O.libm_matches_replica():
+        pytest.skip("host libm is not the glibc FMA variant the device replicates")
+    dc, oc = cfg_pair(**{**kw, "episode_length": min(kw.get("episode_length", 500), 20)})
+    ws = W.Workspace(dc, envs, reference=True)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, oc.seed)
+    o = O.OracleWorld(oc, envs)
+    assert_same(dev_snapshot(ws, o.layout), o.snapshot(), "twin registration")
+    rng = np.random.default_rng(2)
+    A, C, V = dc.num_agents(), dc.action_categories(), dc.action_choices()
+    steps = 30 if A < 500 else 8
+    for t in range(steps):
+        lg = rng.normal(0, 2, (envs, A, C, V))
+        d_lg = to_dev(lg)
+        drv.set_logits(d_lg, lg.size)
+        drv.step()
+        o.rollout(t, 1, oc.seed, lg)
+        assert_same(dev_snapshot(ws, o.layout), o.snapshot(), f"twin step {t}")
+    for e in range(envs):
+        assert ws.resets.episodes_started(e) == o.episodes(e)
     ws.close()
 
 

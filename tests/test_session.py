@@ -101,6 +101,8 @@ def test_session_modes_on_device(tmp_path):
         ("discrete", "full"), ("discrete", "partial"), ("continuous", "full"), ("continuous", "partial")}
     assert rep["meta"]["config_hash"] == s.config_hash() and rep["meta"]["mode"] == "check"
     assert s.summary().startswith("check: PASS (4/4 combos)")
+    # both legs ran: production plan vs the device TagReference twin, fused vs unfused
+    assert all(c["legs"]["reference"]["passed"] and c["legs"]["fused"]["passed"] for c in rep["combos"])
     assert (tmp_path / "check.csv").exists() and (tmp_path / "report.json").exists()
     s.dump_array("observations", str(tmp_path / "obs.csv"))
     lines = (tmp_path / "obs.csv").read_text().splitlines()
@@ -116,4 +118,35 @@ def test_session_modes_on_device(tmp_path):
     assert len(rep["rows"]) == 4 and set(rep["slopes"]) == {"partial", "full"}
     assert all(r["per_env_step_us"] > 0 for r in rep["rows"])
     assert os.path.exists(tmp_path / "bench_agents.csv")
+    s.close()
+
+
+@pytest.mark.gpu
+def test_session_check_catches_fault_hook(tmp_path):
+    """Mutation test of the device check: the fault hook biases
+    the production plan's tag radius only; the independent TagReference twin
+    is unaffected, so the reference leg reports the first divergence, in
+    rewards, as the reference's checker does (harness.cpp:619-629)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    cfg = {"env": {"num_taggers": 2, "num_runners": 10, "k_nearest": 5, "episode_length": 100, "seed": 1},
+           "engine": {"num_envs": 60}, "trainer": {"seed": 4},
+           "run": {"check_steps": 100, "output_dir": str(tmp_path)}}
+    s = W.Session(json.dumps(cfg))
+    W.set_fault_tag_radius_bias(1.0)
+    try:
+        with pytest.raises(W.WarpError) as ei:  # a failed check is WD_ERR_STATE (c_api.cpp:205-212)
+            s.run_check()
+        assert ei.value.code == W.STATE
+    finally:
+        W.set_fault_tag_radius_bias(0.0)
+    rep = json.loads(s.report_json())
+    assert rep["passed"] is False
+    failing = [c for c in rep["combos"] if not c["passed"]]
+    assert failing
+    for c in failing:
+        assert c["divergence"]["leg"] == "reference"
+        assert c["divergence"]["array"] == "rewards"
+    assert "FAIL" in s.summary()
     s.close()
