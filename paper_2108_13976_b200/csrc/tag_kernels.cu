@@ -1170,25 +1170,34 @@ constexpr int env_min_blocks(bool cont, int maxk) {
 // single-step one compiles the step loop away (one iteration known at compile
 // time), which keeps its code identical to a loop-free kernel — measured 35%
 // fewer instructions on the full-observation writer than the looped build.
-template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT, bool MULTI>
+// LEAN: the lattice instantiation of the partial-observation step (discrete,
+// K = 5 staged rows, one env per CTA, A % 4 == 0, bulk-staged inputs, lattice
+// cells, single step, step/fused modes — launch_variant checks all of it). The
+// same body with those facts compile-time: the generic layouts and the
+// multi-step loop drop out (the per-agent K-NN fallback for pushed off-lattice
+// positions stays inline: an out-of-line call measured 151 vs 113 us/step, its
+// ABI spills landing on the hot path). Measured at C2: 62 registers without
+// spills instead of 64 with 28 B of spills, 113 vs 132 us/step (A/B on one box).
+template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT, bool MULTI, bool LEAN = false>
 __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK)) tag_env_kernel(const TagDevConfig p, const TagDevArrays g,
                                                        const TagLaunch L) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int tpe = p.threads_per_env;
-  const int le = tid / tpe;
-  const int lt = tid - le * tpe;
+  static_assert(!LEAN || (!CONT && PARTIAL && GRID && EXACT && !MULTI), "LEAN is the lattice single-step case");
+  const int tpe = LEAN ? static_cast<int>(blockDim.x) : p.threads_per_env;
+  const int le = LEAN ? 0 : tid / tpe;
+  const int lt = LEAN ? tid : tid - le * tpe;
   const int64_t e = static_cast<int64_t>(blockIdx.x) * p.envs_per_cta + le;
   const bool env_ok = le < p.envs_per_cta && e < p.E;
-  const int mode = L.mode;
+  const int mode = LEAN ? (L.mode == kModeStep ? kModeStep : kModeFused) : L.mode;
   const int A = p.A;
   // Fused steps sample from L.logits; with L.logits == nullptr the actions are
   // already in the store (sampled by the policy kernel) and are read like the
   // step mode does.
   const bool sample_here = mode == kModeFused && L.logits != nullptr;
-  const bool single = p.envs_per_cta == 1;  // CTA == one env: warp collectives are per env
+  const bool single = LEAN || p.envs_per_cta == 1;  // CTA == one env: warp collectives are per env
   // Tag action space (tag_env.hpp:48-63): discrete C=1 x V=5, continuous C=2 x V=3.
   constexpr int kC = CONT ? 2 : 1;
   constexpr int kV = CONT ? 3 : 5;
@@ -1272,9 +1281,9 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   // Single-env CTAs with A % 4 == 0 move 4 consecutive agents per thread in
   // the per-agent phases so every global access is a 16-byte (or 4-byte for
   // flags) vector and the logits rows of a thread are contiguous.
-  const bool vec4 = GRID && (A & 3) == 0;
+  const bool vec4 = GRID && (LEAN || (A & 3) == 0);
 
-  const int n_steps = MULTI && mode == kModeFused && sample_here ? L.n_steps : 1;
+  const int n_steps = !LEAN && MULTI && mode == kModeFused && sample_here ? L.n_steps : 1;
   for (int it = 0; it < n_steps; ++it) {
   // Iteration `it` of a multi-step launch: step L.step0 + it. After the first,
   // the env's state is already in shared memory (written by the previous
@@ -1297,7 +1306,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     // bulk copies of the env's contiguous rows — f64 logits (fused) into the
     // zone, positions (+ speed/direction) straight into their smem arrays —
     // so the whole 40-50 KB input is in flight at once with no registers held.
-    const bool bulk = p.bulk_in != 0;
+    const bool bulk = LEAN || p.bulk_in != 0;
     const double* zone = reinterpret_cast<const double*>(smem + p.off_zone);
     if (bulk) {
       uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.envs_per_cta * sizeof(EnvScalars) + kScratchDoubles * 8);
@@ -1943,16 +1952,18 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
                                [&](int n) { return static_cast<int>(lst[n + (n >= self_pos ? 1 : 0)]); });
           }
         } else if (PARTIAL && s.act[a]) {
-          TopK<MAXK, EXACT> top;
-          knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top, brute_keys, disc_integral);
-          write_row<CONT, (EXACT ? MAXK : 0)>(s, p, sc.step_count, a, row, [&](int n) {
-            int j = top.i[0];
+          {
+            TopK<MAXK, EXACT> top;
+            knn_agent<CONT, GRID, MAXK, EXACT>(s, p, a, lattice_ok, top, brute_keys, disc_integral);
+            write_row<CONT, (EXACT ? MAXK : 0)>(s, p, sc.step_count, a, row, [&](int n) {
+              int j = top.i[0];
 #pragma unroll
-            for (int t = 1; t < MAXK; ++t)
-              if (t == n) j = top.i[t];
-            return j;
-          });
-        } else {
+              for (int t = 1; t < MAXK; ++t)
+                if (t == n) j = top.i[t];
+              return j;
+            });
+          }
+        } else if constexpr (!PARTIAL) {
           write_row<CONT, 0>(s, p, sc.step_count, a, row, [&](int n) { return n < a ? n : n + 1; });
         }
       }
@@ -2242,6 +2253,12 @@ cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const T
   // 6-35% slower there.
   auto kern = (L.n_steps > 1 || PARTIAL) ? tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, true>
                                          : tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, false>;
+  if constexpr (!CONT && PARTIAL && GRID && EXACT) {
+    // the lattice single step (see LEAN at tag_env_kernel)
+    const bool lean = L.mode >= 0 && L.mode != kModeReinit && L.n_steps <= 1 && p.envs_per_cta == 1 &&
+                      (p.A & 3) == 0 && p.bulk_in && p.lattice && p.threads_per_env == p.threads;
+    if (lean) kern = tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, false, true>;
+  }
   if (L.mode < 0) {  // occupancy query (kModeQuery): resident CTAs per SM -> *L.error
     if (p.smem_bytes > 48 * 1024) {
       cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);

@@ -13,10 +13,9 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 cfg = W.TagConfig(num_taggers=200, num_runners=800, obs_mode=W.PARTIAL, k_nearest=5, episode_length=40, seed=7)
 ws1 = W.Workspace(cfg, 2000)
 d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 3)
-os.environ["WDG_NO_PDL"] = "1"
 ws2 = W.Workspace(cfg, 2000)
 d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 3)
-del os.environ["WDG_NO_PDL"]
+d2.set_overlap(False)
 for d in (d1, d2):
     for _ in range(n):
         d.step()

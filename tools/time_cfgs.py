@@ -24,9 +24,9 @@ for name in (sys.argv[1:] or list(SHAPES)):
         T = 1
     cfg = W.TagConfig(variant=var, num_taggers=T, num_runners=A - T, obs_mode=W.PARTIAL if K else W.FULL,
                       k_nearest=K or 5)
-    os.environ["WDG_NO_MULTISTEP"] = "1"
+    W.set_tuning("multistep", 0)
     sps1, ms1, _ = measure(cfg, E, 200, warmup=5)
-    del os.environ["WDG_NO_MULTISTEP"]
+    W.set_tuning("multistep", -1)
     sps2, ms2, _ = measure(cfg, E, 200, warmup=5)
     # RolloutDriver::step loop (the bench's per-step launches)
     import torch
