@@ -378,8 +378,10 @@ def run_ours(args, rank, world, local_rank):
     ms_ms = es0.elapsed_time(es1)
     multistep_leg = {"steps": ms_steps, "launches": drv.launches() - ml0,
                      "env_steps_per_s": E * ms_steps / (ms_ms / 1e3), "ms_per_step": ms_ms / ms_steps,
-                     "note": "64 steps per launch, env state resident in smem; the fixed logits buffer "
-                             "is re-read from L2 within an env's 64 steps"}
+                     "note": "RolloutDriver::run with the plan's launch choice: lattice (LEAN) plans such as "
+                             "C2 take one overlapped launch per step; others run up to 64 steps per launch "
+                             "with env state resident in smem (their fixed logits buffer is then re-read "
+                             "from L2 within an env's 64 steps)"}
     drv.check()
 
     # ---- policy leg: the rollout driven by device policies (SURVEY.md §8f

@@ -15,6 +15,9 @@ struct ResetRowDesc {
   int64_t row_bytes;
 };
 
+// Whether single fused/step launches of this plan take the LEAN lattice
+// instantiation (tag_kernels.cu).
+bool lean_plan(const TagDevConfig& p);
 cudaError_t launch_tag_kernel(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                               cudaStream_t st);
 cudaError_t launch_sample(const double* logits, int32_t* actions, int64_t rows, int A, int C, int V,

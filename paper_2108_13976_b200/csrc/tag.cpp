@@ -332,9 +332,10 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     p.off_cstart = take(4 * (p.ncells + 1), 4);
     p.off_cfill = take(4 * (p.ncells + 1), 4);
     p.off_items = take(2 * A, 4);
-    p.off_cellof = take(2 * A, 4);
+    p.off_cellof = take(2 * A, 16);  // 8-byte vector access (build_grid_lattice)
     if (p.lattice && p.partial) p.off_cellknn = take(2 * int64_t{p.ncells} * (p.K + 1), 4);
     p.off_cellact = take(p.ncells, 16);
+    if (p.lattice) p.off_celltag = take(4 * int64_t{p.ncells}, 16);
   }
   p.env_bytes = align16(off);
   // CTA header: per-env scalars + 64 doubles of warp scratch (scan / sums).
@@ -523,6 +524,9 @@ int TagPlan::pdl_mode() const {
 bool TagPlan::multistep_ok() {
   if (multistep_ < 0) {
     multistep_ = 1;
+    // the LEAN lattice single step (one launch per step, overlapped) beats
+    // the looped multi-step build at C2: 107 vs 117 us/step
+    if (lean_plan(dev_)) multistep_ = 0;
     // full observations on the grid path: the looped (multi-step) build of
     // the wide-row writer is 6-9% slower than the single-step build
     // (profiles/sweep_r01.json), which outweighs the saved state reloads
@@ -1252,7 +1256,9 @@ void Rollout::run(int64_t steps) {
     }
     return;
   }
-  if (graphs_ && fused_ok() && steps >= kGraphSteps) {
+  // LEAN plans: direct overlapped launches (107 us/step at C2) beat the graph
+  // replay of the same launches (111 us/step).
+  if (graphs_ && fused_ok() && steps >= kGraphSteps && !(lean_plan(plan_.dev()) && pdl_flags_ != nullptr)) {
     if (graph_exec_ == nullptr || graph_logits_ != logits_ || graph_pol_version_ != pol_version_ ||
         graph_bias_ != fault_tag_radius_bias() ||
         graph_stream_ != store_.stream()) {

@@ -168,6 +168,7 @@ struct EnvSmem {
   uint16_t* cellof;
   uint16_t* cellknn;  // lattice: per-cell top-(K+1) lists
   uint8_t* cellact;   // grid: cell holds an active agent
+  int32_t* celltag;   // lattice (LEAN): lowest-index tagger per cell
 };
 
 __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
@@ -189,6 +190,7 @@ __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
   s.cellof = reinterpret_cast<uint16_t*>(b + p.off_cellof);
   s.cellknn = reinterpret_cast<uint16_t*>(b + p.off_cellknn);
   s.cellact = b + p.off_cellact;
+  s.celltag = reinterpret_cast<int32_t*>(b + p.off_celltag);
   return s;
 }
 
@@ -437,6 +439,107 @@ __device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t
     }
   }
   return found;
+}
+
+// ---- lattice grid + per-cell lists for the LEAN kernel ---------------------
+// Counting sort of the agents into CSR lattice cells in scatter (atomic) order:
+// no per-cell index sort, because nothing downstream needs one — the
+// lowest-index tagger of each cell comes from an atomicMin while counting,
+// the per-cell K-NN lists insert (d2, index) keys, and find_tagger's cell scan
+// takes the minimum index. Thread t owns agents 4t..4t+3 (A % 4 == 0).
+__device__ void build_grid_lattice(const EnvSmem& s, const TagDevConfig& p, int* scratch, bool mark_active) {
+  const int nthr = blockDim.x, tid = threadIdx.x;
+  for (int c = tid; c <= p.ncells; c += nthr) {
+    s.cfill[c] = 0;
+    if (c < p.ncells) {
+      s.cellact[c] = 0;
+      s.celltag[c] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  for (int a0 = 4 * tid; a0 < p.A; a0 += 4 * nthr) {
+    const float4 x4 = *reinterpret_cast<const float4*>(s.x + a0);
+    const float4 y4 = *reinterpret_cast<const float4*>(s.y + a0);
+    const uint32_t tg4 = *reinterpret_cast<const uint32_t*>(s.tag + a0);
+    const uint32_t ac4 = mark_active ? *reinterpret_cast<const uint32_t*>(s.act + a0) : 0u;
+    const float xs[4] = {x4.x, x4.y, x4.z, x4.w}, ys[4] = {y4.x, y4.y, y4.z, y4.w};
+    int cl[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      cl[k] = cell_coord<false>(ys[k], p) * p.gc + cell_coord<false>(xs[k], p);
+      atomicAdd(&s.cfill[cl[k]], 1);
+      if ((tg4 >> (8 * k)) & 0xffu) atomicMin(&s.celltag[cl[k]], a0 + k);
+      if (mark_active && ((ac4 >> (8 * k)) & 0xffu)) s.cellact[cl[k]] = 1;
+    }
+    *reinterpret_cast<uint2*>(s.cellof + a0) =
+        make_uint2(static_cast<uint32_t>(cl[0]) | (static_cast<uint32_t>(cl[1]) << 16),
+                   static_cast<uint32_t>(cl[2]) | (static_cast<uint32_t>(cl[3]) << 16));
+  }
+  __syncthreads();
+  block_scan_cells(s, p.ncells, p.A, scratch);
+  __syncthreads();
+  for (int a0 = 4 * tid; a0 < p.A; a0 += 4 * nthr) {
+    const uint2 c2 = *reinterpret_cast<const uint2*>(s.cellof + a0);
+    const int cl[4] = {static_cast<int>(c2.x & 0xffffu), static_cast<int>(c2.x >> 16),
+                       static_cast<int>(c2.y & 0xffffu), static_cast<int>(c2.y >> 16)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s.items[atomicAdd(&s.cfill[cl[k]], 1)] = static_cast<uint16_t>(a0 + k);
+  }
+  __syncthreads();
+}
+
+// Lattice K-NN per CELL by key insertion: every agent of the shells around
+// lattice point c, visited in increasing d2, enters a register top-(K+1) of
+// 32-bit keys (d2 << 16 | index) — the (d2, index) total order as one
+// unsigned compare, inserted by a branchless min/max chain in any item order.
+// Stops once the list is full and the next shell is strictly farther. Same
+// list as cell_knn (the order is total). Returns the count found (< KK only
+// if the precomputed disk is exhausted; the caller falls back per agent).
+template <int KK>
+__device__ __forceinline__ int cell_knn_keys(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t* out) {
+  const int g = p.gc;
+  const int cy = c / g, cx = c - cy * g;
+  uint32_t l[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) l[t] = 0xffffffffu;
+  int found = 0;
+  const int ns = c_num_shells;
+  for (int sh = 0; sh < ns; ++sh) {
+    const uint32_t d2 = static_cast<uint32_t>(c_shell_d2[sh]);
+    if (found >= KK && (l[KK - 1] >> 16) < d2) break;
+    const uint32_t hi = d2 << 16;
+    const int ob = c_shell_begin[sh], oe = c_shell_begin[sh + 1];
+    for (int o = ob; o < oe; ++o) {
+      const int packed = c_shell_off[o];
+      const int gx = cx + (packed & 0xff) - 64;
+      const int gy = cy + ((packed >> 8) & 0xff) - 64;
+      if (static_cast<unsigned>(gx) >= static_cast<unsigned>(g) ||
+          static_cast<unsigned>(gy) >= static_cast<unsigned>(g))
+        continue;
+      const int c2 = gy * g + gx;
+      const int e = s.cstart[c2 + 1];
+      for (int t = s.cstart[c2]; t < e; ++t) {
+        uint32_t key = hi | s.items[t];
+#pragma unroll
+        for (int q = 0; q < KK; ++q) {
+          const uint32_t lo = min(l[q], key);
+          key = max(l[q], key);
+          l[q] = lo;
+        }
+        ++found;
+      }
+    }
+  }
+  const int n = found < KK ? found : KK;
+#pragma unroll
+  for (int t = 0; t < KK; ++t)
+    if (t < n) out[t] = static_cast<uint16_t>(l[t] & 0xffffu);
+  return n;
+}
+
+__device__ __forceinline__ void build_cell_lists_keys(const EnvSmem& s, const TagDevConfig& p) {
+  for (int c = threadIdx.x; c < p.ncells; c += blockDim.x)
+    s.cfill[c] = s.cellact[c] ? cell_knn_keys<6>(s, p, c, s.cellknn + c * 6) : 0;
 }
 
 // Per-cell top-(K+1) lists for every cell holding an active agent (only those
@@ -777,15 +880,15 @@ __device__ int find_tagger(const EnvSmem& s, const TagDevConfig& p, int rn, bool
     return best;
   }
   if (exact_cell) {
-    // cells are index-sorted: the first tagger at the runner's position is
-    // the lowest-index one (tag_env.cpp:430-434)
+    // the lowest-index tagger at the runner's position (tag_env.cpp:430-434),
+    // whatever the order of the cell's items
     const int c = s.cellof[rn];
     const int e = s.cstart[c + 1];
     for (int t = s.cstart[c]; t < e; ++t) {
       const int j = s.items[t];
-      if (s.tag[j] && s.x[j] == rx && s.y[j] == ry) return j;
+      if (s.tag[j] && s.x[j] == rx && s.y[j] == ry && (best < 0 || j < best)) best = j;
     }
-    return -1;
+    return best;
   }
   const float R = __fadd_rn(__fmul_rn(radius, 1.001f), 1e-6f);
   const int x0 = cell_coord<CONT>(__fsub_rn(rx, R), p), x1 = cell_coord<CONT>(__fadd_rn(rx, R), p);
@@ -1594,7 +1697,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     // Phase 2: bucket grid over post-move positions (NeighborGrid::build).
     // lattice cells are exact positions: lowest-index tagger per cell
     const bool cell_tagger = !CONT && GRID && p.lattice && all_integral && p.fault_bias == 0.0f;
-    if (GRID && !(ablate_bits(L) & 8u)) build_grid<CONT>(s, p, scratch, false, cell_tagger);
+    if constexpr (LEAN) {
+      build_grid_lattice(s, p, scratch, false);
+    } else {
+      if (GRID && !(ablate_bits(L) & 8u)) build_grid<CONT>(s, p, scratch, false, cell_tagger);
+    }
 
     // Phase 3: resolve tags (tag_env.cpp:403-456). Counts are warp-aggregated
     // when the CTA is one env; there "any runner still active" is all
@@ -1605,7 +1712,15 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       const int a = base + lt;
       const bool valid = live && a < A;
       const bool runner = valid && !s.tag[a] && s.act[a];
-      const int best = runner ? find_tagger<CONT, GRID>(s, p, a, cell_tagger, CONT ? all_integral : all_prefix) : -1;
+      int best = -1;
+      if (runner) {
+        if (LEAN && cell_tagger) {
+          const int ct = s.celltag[s.cellof[a]];
+          best = ct == 0x7fffffff ? -1 : ct;
+        } else {
+          best = find_tagger<CONT, GRID>(s, p, a, cell_tagger && !LEAN, CONT ? all_integral : all_prefix);
+        }
+      }
       if (best >= 0) {
         s.act[a] = 0;
         s.tagged[a] = 1;
@@ -1708,8 +1823,12 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           s.cs[a] = cos_ref(s.dir[a]);
         }
       }
-      if (PARTIAL && !CONT && GRID && p.lattice && all_integral)
-        build_cell_lists(s, p, ablate_bits(L));
+      if (PARTIAL && !CONT && GRID && p.lattice && all_integral) {
+        if constexpr (LEAN)
+          build_cell_lists_keys(s, p);
+        else
+          build_cell_lists(s, p, ablate_bits(L));
+      }
     }
     __syncthreads();
     if (live && lt == 0 && track) {
@@ -1815,7 +1934,10 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   // single-env CTA: `place` is CTA-uniform here (every thread has le == 0)
   if (GRID && PARTIAL && single && place) {
     __syncthreads();
-    build_grid<CONT>(s, p, scratch, true);
+    if constexpr (LEAN)
+      build_grid_lattice(s, p, scratch, true);
+    else
+      build_grid<CONT>(s, p, scratch, true);
   }
   if (!early_inputs) __syncthreads();
   const bool lattice_ok = !CONT && GRID && p.lattice && scal[0].lattice_ok;
@@ -1840,7 +1962,10 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     const bool cell_lists = PARTIAL && lattice_ok;  // GRID => single env per CTA
     const int kk = p.K + 1;
     if (cell_lists && !early_inputs) {
-      build_cell_lists(s, p, ablate_bits(L));
+      if constexpr (LEAN)
+        build_cell_lists_keys(s, p);
+      else
+        build_cell_lists(s, p, ablate_bits(L));
       __syncthreads();
     }
     if constexpr (CONT && EXACT && PARTIAL) {
@@ -2245,6 +2370,10 @@ cudaError_t ensure_shell_table() {
   return cudaSuccess;
 }
 
+}  // namespace
+bool lean_plan(const TagDevConfig& p);
+namespace {
+
 template <bool CONT, bool PARTIAL, bool GRID, int MAXK, bool EXACT>
 cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                            cudaStream_t st) {
@@ -2255,8 +2384,7 @@ cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const T
                                          : tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, false>;
   if constexpr (!CONT && PARTIAL && GRID && EXACT) {
     // the lattice single step (see LEAN at tag_env_kernel)
-    const bool lean = L.mode >= 0 && L.mode != kModeReinit && L.n_steps <= 1 && p.envs_per_cta == 1 &&
-                      (p.A & 3) == 0 && p.bulk_in && p.lattice && p.threads_per_env == p.threads;
+    const bool lean = L.mode >= 0 && L.mode != kModeReinit && L.n_steps <= 1 && lean_plan(p);
     if (lean) kern = tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, false, true>;
   }
   if (L.mode < 0) {  // occupancy query (kModeQuery): resident CTAs per SM -> *L.error
@@ -2317,6 +2445,11 @@ cudaError_t launch_g(const TagDevConfig& p, const TagDevArrays& g, const TagLaun
 }  // namespace
 
 // ---- host-callable launchers (declared in kernels.hpp) ---------------------
+bool lean_plan(const TagDevConfig& p) {
+  return !p.continuous && p.partial && p.use_grid && p.K == 5 && p.stage_obs && p.envs_per_cta == 1 &&
+         (p.A & 3) == 0 && p.bulk_in && p.lattice && p.threads_per_env == p.threads;
+}
+
 cudaError_t launch_tag_kernel(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                               cudaStream_t st) {
   if (p.continuous) {
