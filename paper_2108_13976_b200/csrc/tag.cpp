@@ -335,7 +335,10 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     p.off_cellof = take(2 * A, 16);  // 8-byte vector access (build_grid_lattice)
     if (p.lattice && p.partial) p.off_cellknn = take(2 * int64_t{p.ncells} * (p.K + 1), 4);
     p.off_cellact = take(p.ncells, 16);
-    if (p.lattice) p.off_celltag = take(4 * int64_t{p.ncells}, 16);
+    if (p.lattice) {
+      p.off_celltag = take(4 * int64_t{p.ncells}, 16);
+      p.off_cellq = take(2 * int64_t{p.ncells}, 16);
+    }
   }
   p.env_bytes = align16(off);
   // CTA header: per-env scalars + 64 doubles of warp scratch (scan / sums).

@@ -169,6 +169,7 @@ struct EnvSmem {
   uint16_t* cellknn;  // lattice: per-cell top-(K+1) lists
   uint8_t* cellact;   // grid: cell holds an active agent
   int32_t* celltag;   // lattice (LEAN): lowest-index tagger per cell
+  uint16_t* cellq;    // lattice (LEAN): compacted active cells
 };
 
 __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
@@ -191,6 +192,7 @@ __device__ __forceinline__ EnvSmem carve(uint8_t* b, const TagDevConfig& p) {
   s.cellknn = reinterpret_cast<uint16_t*>(b + p.off_cellknn);
   s.cellact = b + p.off_cellact;
   s.celltag = reinterpret_cast<int32_t*>(b + p.off_celltag);
+  s.cellq = reinterpret_cast<uint16_t*>(b + p.off_cellq);
   return s;
 }
 
@@ -447,8 +449,11 @@ __device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t
 // lowest-index tagger of each cell comes from an atomicMin while counting,
 // the per-cell K-NN lists insert (d2, index) keys, and find_tagger's cell scan
 // takes the minimum index. Thread t owns agents 4t..4t+3 (A % 4 == 0).
+constexpr int kCellQCount = 64;  // scratch int slot: build_cell_lists_keys' queue length
+
 __device__ void build_grid_lattice(const EnvSmem& s, const TagDevConfig& p, int* scratch, bool mark_active) {
   const int nthr = blockDim.x, tid = threadIdx.x;
+  if (tid == 0) scratch[kCellQCount] = 0;
   for (int c = tid; c <= p.ncells; c += nthr) {
     s.cfill[c] = 0;
     if (c < p.ncells) {
@@ -537,9 +542,28 @@ __device__ __forceinline__ int cell_knn_keys(const EnvSmem& s, const TagDevConfi
   return n;
 }
 
-__device__ __forceinline__ void build_cell_lists_keys(const EnvSmem& s, const TagDevConfig& p) {
-  for (int c = threadIdx.x; c < p.ncells; c += blockDim.x)
-    s.cfill[c] = s.cellact[c] ? cell_knn_keys<6>(s, p, c, s.cellknn + c * 6) : 0;
+// Lists only for cells holding an active agent, compacted first so every
+// lane of a warp works on one (inactive agents observe zeros; tagged runners
+// leave many cells without an active agent). The queue length lives in
+// scratch[kCellQCount], zeroed by build_grid_lattice.
+__device__ __forceinline__ void build_cell_lists_keys(const EnvSmem& s, const TagDevConfig& p, int* scratch) {
+  const int lane = threadIdx.x & 31;
+  for (int c0 = threadIdx.x & ~31; c0 < p.ncells; c0 += blockDim.x) {
+    const int c = c0 + lane;
+    const bool act = c < p.ncells && s.cellact[c];
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(&scratch[kCellQCount], __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (act) s.cellq[base + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(c);
+    else if (c < p.ncells) s.cfill[c] = 0;
+  }
+  __syncthreads();
+  const int n = scratch[kCellQCount];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int c = s.cellq[i];
+    s.cfill[c] = cell_knn_keys<6>(s, p, c, s.cellknn + c * 6);
+  }
 }
 
 // Per-cell top-(K+1) lists for every cell holding an active agent (only those
@@ -1825,7 +1849,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       }
       if (PARTIAL && !CONT && GRID && p.lattice && all_integral) {
         if constexpr (LEAN)
-          build_cell_lists_keys(s, p);
+          build_cell_lists_keys(s, p, scratch);
         else
           build_cell_lists(s, p, ablate_bits(L));
       }
@@ -1963,7 +1987,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     const int kk = p.K + 1;
     if (cell_lists && !early_inputs) {
       if constexpr (LEAN)
-        build_cell_lists_keys(s, p);
+        build_cell_lists_keys(s, p, scratch);
       else
         build_cell_lists(s, p, ablate_bits(L));
       __syncthreads();

@@ -92,6 +92,7 @@ struct TagDevConfig {
   int32_t off_cstart = 0, off_cfill = 0, off_items = 0, off_cellof = 0, off_cellknn = 0;
   int32_t off_cellact = 0;  // grid: per-cell "holds an active agent" flags
   int32_t off_celltag = 0;  // discrete lattice: per-cell lowest-index tagger (int32, INT_MAX = none)
+  int32_t off_cellq = 0;    // discrete lattice: compacted list of the cells holding an active agent
   int32_t head_bytes = 0;         // CTA header (per-env scalars + scan scratch + mbarrier)
   int32_t bulk_in = 0;            // fused/step inputs staged by TMA bulk copies (one env per CTA)
   int32_t off_zone = 0;           // CTA offset of the bulk logits landing zone
