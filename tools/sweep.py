@@ -49,6 +49,40 @@ def measure(cfg, envs, steps, warmup=10, graphs=True, check=True):
     return envs * steps / (ms / 1e3), ms / steps, geo
 
 
+def launch_floor(n=2000):
+    """The C4 floor: per-launch time of an empty kernel
+    (torch.cuda._sleep(0)) launched back to back, and per node of a CUDA graph
+    of such nodes (each kernel waits for the previous: the stream order every
+    Tag step has)."""
+    st = torch.cuda.current_stream()
+    for _ in range(50):
+        torch.cuda._sleep(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(n):
+        torch.cuda._sleep(0)
+    e1.record(st)
+    torch.cuda.synchronize()
+    direct = e0.elapsed_time(e1) * 1e3 / n
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(g, stream=cap):
+            for _ in range(64):
+                torch.cuda._sleep(0)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record(st)
+    reps = max(1, n // 64)
+    for _ in range(reps):
+        g.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    graph = e0.elapsed_time(e1) * 1e3 / (reps * 64)
+    return {"empty_kernel_us": direct, "graph_node_us": graph}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=500)
@@ -69,13 +103,24 @@ def main():
                              ms_per_step=ms, per_env_step_us=1e3 * ms / 2000, algo_GBps=gbs,
                              hbm_frac=gbs / hbm_peak(), geometry=geo))
             print(json.dumps(rows[-1]))
-    # C4: env sweep, 5 agents (1 tagger + 4 runners), full obs D=19
+    # C4: env sweep, 5 agents (1 tagger + 4 runners), full obs D=19. The
+    # working set fits in L2, so the bound is launch latency: each row also
+    # reports the empty-kernel floor and the step's multiple of it.
+    floor = launch_floor()
+    rows.append(dict(sweep="launch floor", **floor))
+    print(json.dumps(rows[-1]))
     for E in (1, 10, 100, 1000, 2000, 5000, 10000):
         cfg = W.TagConfig(num_taggers=1, num_runners=4)
+        W.set_tuning("multistep", 0)  # one launch per step (graph replay): the single-step latency
+        sps1, ms1, _ = measure(cfg, E, args.steps)
+        W.set_tuning("multistep", -1)
         sps, ms, geo = measure(cfg, E, args.steps)
         gbs = sps * algo_bytes(cfg) / 1e9
         rows.append(dict(sweep="C4 envs", agents=5, envs=E, obs="full", env_steps_per_s=sps,
-                         ms_per_step=ms, algo_GBps=gbs, hbm_frac=gbs / hbm_peak(), geometry=geo))
+                         ms_per_step=ms, single_step_us=1e3 * ms1, run_step_us=1e3 * ms,
+                         floor_graph_node_us=floor["graph_node_us"],
+                         single_step_vs_floor=1e3 * ms1 / floor["graph_node_us"],
+                         algo_GBps=gbs, hbm_frac=gbs / hbm_peak(), geometry=geo))
         print(json.dumps(rows[-1]))
     # Continuous Tag (paper: 2000 envs x 5 agents) and larger A
     for A, mode, name in ((5, W.FULL, "full"), (100, W.PARTIAL, "partial"), (1000, W.PARTIAL, "partial")):
