@@ -18,6 +18,9 @@ struct ResetRowDesc {
 // Whether single fused/step launches of this plan take the LEAN lattice
 // instantiation (tag_kernels.cu).
 bool lean_plan(const TagDevConfig& p);
+// Whether fused launches of this plan (no overlap flags, no capture) take the
+// warp-resident small-env kernel (A <= 32, tag_kernels.cu).
+bool small_plan(const TagDevConfig& p);
 cudaError_t launch_tag_kernel(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                               cudaStream_t st);
 cudaError_t launch_sample(const double* logits, int32_t* actions, int64_t rows, int A, int C, int V,

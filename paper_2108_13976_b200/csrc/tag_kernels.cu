@@ -2263,6 +2263,318 @@ obs_done:
   }
 }
 
+// ---- SMALL: warp-resident small envs (A <= 32) -----------------------------
+// RolloutDriver::step (harness.cpp:478-490) for envs of at most 32 agents
+// (C4's 1 + 4, C3's A = 10): each env is a segment of A lanes of one warp,
+// one agent per lane, and the whole step runs in registers with no shared
+// memory and no barrier — neighbours' positions and flags come by
+// __shfl_sync, per-env counters by segment ballots. A launch runs n_steps
+// steps with the state in registers (RolloutDriver::run); every step still
+// reads its logits and writes every output. The latency-bound packed path of
+// tag_env_kernel spent ~1,400 dependent instructions per step per warp on
+// shared-memory round trips and CTA barriers (profiles/ncu_r02_c4_e2000_v1.md).
+// Same arithmetic as the main kernel (sample_tag_row, move_regs, d2_of, the
+// write_obs_row formulas, the fused reset), so results are bit-identical.
+constexpr int kSmallThreads = 64;
+
+template <bool CONT, bool PARTIAL, int MAXK>
+__global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevConfig p, const TagDevArrays g,
+                                                                  const TagLaunch L) {
+  constexpr int kC = CONT ? 2 : 1;
+  constexpr int kV = CONT ? 3 : 5;
+  constexpr int NBF = CONT ? 7 : 4;
+  extern __shared__ __align__(16) float small_stage[];
+  const int lane = threadIdx.x & 31;
+  const int A = p.A;
+  const int epw = 32 / A;  // envs per warp
+  float* stage = small_stage + (threadIdx.x >> 5) * (epw * A * p.D);
+  auto st_sm = [](float* q, float v) { *q = v; };
+  const int le = lane / A, la = lane - le * A;
+  const int64_t wg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t e = wg * epw + le;
+  const bool valid = le < epw && e < p.E;
+  const int base = le * A;  // first lane of this env's segment
+  const unsigned seg = valid ? ((A == 32 ? 0xffffffffu : ((1u << A) - 1u)) << base) : 0u;
+  if (L.pdl_wait) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  const int64_t ga = e * A;
+  const int64_t ia = ga + la;
+  float x = 0.f, y = 0.f, sp = 0.f, dir = 0.f;
+  bool act = false, tag = false;
+  int32_t step_count = 0, episode = 0;
+  double es[4] = {0.0, 0.0, 0.0, 0.0};  // env_stats [0], [1], [5], [6] (held by the env's lane 0)
+  if (valid) {
+    x = g.loc_x[ia];
+    y = g.loc_y[ia];
+    if (CONT) {
+      sp = g.speed[ia];
+      dir = g.direction[ia];
+    }
+    act = g.active[ia] != 0;
+    tag = g.is_tagger[ia] != 0;
+    step_count = g.step_count[e];
+    episode = L.episode != nullptr ? L.episode[e] : 0;
+    if (la == 0 && L.track) {
+      const double* s8 = L.env_stats + e * 8;
+      es[0] = s8[0];
+      es[1] = s8[1];
+      es[2] = s8[5];
+      es[3] = s8[6];
+    }
+  }
+  bool nonfinite = false;
+  const bool sample_here = L.logits != nullptr;
+  const int n_steps = L.n_steps > 1 ? L.n_steps : 1;
+  const float bias = p.fault_bias;
+  const bool exact_cell = !CONT && bias == 0.0f;
+  const float radius = CONT ? __fadd_rn(p.tag_radius, bias) : bias;
+  const float r2 = __fmul_rn(radius, radius);
+  for (int it = 0; it < n_steps; ++it) {
+    // sample (sampler.cpp:5-40) + apply_move (tag_env.cpp:148-160)
+    int32_t act0 = 0, act1 = 1;
+    if (valid) {
+      const int64_t row = ia * kC;
+      if (sample_here) {
+        const uint64_t h_step =
+            n_steps > 1 ? absorb(L.action_h0, static_cast<uint64_t>(L.step0 + it))
+            : L.step_dev != nullptr
+                ? absorb(L.action_h0, static_cast<uint64_t>(*L.step_dev + static_cast<int64_t>(L.step_add)))
+                : L.action_h_step;
+        const uint64_t h_ag = absorb(absorb(h_step, static_cast<uint64_t>(p.env_offset + e)),
+                                     static_cast<uint64_t>(la));
+        act0 = sample_tag_row<kV>(L.logits, row, to_unit(absorb(absorb(h_ag, 0), 0)), nonfinite);
+        g.actions[row] = act0;
+        if (CONT) {
+          act1 = sample_tag_row<kV>(L.logits, row + 1, to_unit(absorb(absorb(h_ag, 1), 0)), nonfinite);
+          g.actions[row + 1] = act1;
+        }
+      } else {
+        act0 = g.actions[row];
+        if (CONT) act1 = g.actions[row + 1];
+      }
+      if (act) move_regs<CONT>(p, la, act0, act1, x, y, sp, dir);
+    }
+    // resolve (tag_env.cpp:403-456 / find_tagger): the lowest-index tagger at
+    // the runner's position (discrete) or min (d2, index) within the radius
+    const bool runner = valid && !tag && act;
+    int best = -1;
+    float best_d2 = 0.0f;
+    for (int j = 0; j < A; ++j) {
+      const float xj = __shfl_sync(0xffffffffu, x, base + j);
+      const float yj = __shfl_sync(0xffffffffu, y, base + j);
+      const bool tj = __shfl_sync(0xffffffffu, tag, base + j);
+      if (!runner || !tj) continue;
+      if (exact_cell) {
+        if (best < 0 && xj == x && yj == y) best = j;
+      } else {
+        const float d2 = d2_of(x, y, xj, yj);
+        if (d2 <= r2 && (best < 0 || d2 < best_d2)) {  // ascending j: ties keep the lower index
+          best = j;
+          best_d2 = d2;
+        }
+      }
+    }
+    const bool tagged = best >= 0;
+    if (tagged) act = false;
+    int credits = 0;
+    for (int j = 0; j < A; ++j) credits += __shfl_sync(0xffffffffu, best, base + j) == la ? 1 : 0;
+    // resolve_env_counters (tag_env.cpp:241-250)
+    const unsigned alive = __ballot_sync(0xffffffffu, runner && !tagged) & seg;
+    const unsigned tags_m = __ballot_sync(0xffffffffu, valid && tagged) & seg;
+    const int32_t step_new = step_count + 1;
+    const bool done_now = step_new >= p.episode_length || alive == 0u;
+    const bool reset_now = valid && L.do_reset && done_now;
+    // rewards (write_rewards_row, tag_env.cpp:252-259) + EpisodeTracker
+    const float r = tag ? __fmul_rn(p.reward_per_tag, static_cast<float>(credits)) : (tagged ? p.penalty : 0.0f);
+    if (valid) {
+      g.rewards[ia] = reset_now ? 0.0f : r;
+      g.credits[ia] = reset_now ? 0 : credits;
+      g.tagged[ia] = (reset_now || !tagged) ? 0 : 1;
+    }
+    if (L.track) {
+      double st = 0.0, sr = 0.0;  // integer-valued: exact in any order
+      for (int j = 0; j < A; ++j) {
+        const double rj = static_cast<double>(__shfl_sync(0xffffffffu, r, base + j));
+        if (j < p.T) st += rj; else sr += rj;
+      }
+      if (valid && la == 0) {
+        double* s8 = L.env_stats + e * 8;
+        const double run_t = es[0] + st, run_r = es[1] + sr;
+        es[2] += static_cast<double>(__popc(tags_m));
+        es[3] += 1.0;
+        s8[5] = es[2];
+        s8[6] = es[3];
+        if (done_now) {
+          s8[2] += 1.0;
+          s8[3] += run_t;
+          s8[4] += run_r;
+          es[0] = es[1] = 0.0;
+        } else {
+          es[0] = run_t;
+          es[1] = run_r;
+        }
+        s8[0] = es[0];
+        s8[1] = es[1];
+      }
+    }
+    step_count = step_new;
+    // fused reset-on-done: re-placement (place_env / place_agent,
+    // tag_env.cpp:130-146,261-273), snapshot is_tagger, zeroed actions
+    if (reset_now) {
+      ++episode;
+      const uint64_t h_ag = absorb(absorb(absorb(p.placement_h0, static_cast<uint64_t>(static_cast<int64_t>(episode))),
+                                          static_cast<uint64_t>(p.env_offset + e)),
+                                   static_cast<uint64_t>(la));
+      const double ux = to_unit(absorb(absorb(h_ag, 0), 0));
+      const double uy = to_unit(absorb(absorb(h_ag, 1), 0));
+      if (!CONT) {
+        const double gd = static_cast<double>(p.grid_size);
+        int64_t ix = static_cast<int64_t>(__dmul_rn(ux, gd));
+        int64_t iy = static_cast<int64_t>(__dmul_rn(uy, gd));
+        ix = ix < p.grid_size - 1 ? ix : p.grid_size - 1;
+        iy = iy < p.grid_size - 1 ? iy : p.grid_size - 1;
+        x = static_cast<float>(ix);
+        y = static_cast<float>(iy);
+      } else {
+        const double ud = to_unit(absorb(absorb(h_ag, 2), 0));
+        x = __double2float_rn(__dmul_rn(ux, p.world_length));
+        y = __double2float_rn(__dmul_rn(uy, p.world_length));
+        dir = __double2float_rn(__dmul_rn(ud, 6.283185307179586));
+        sp = 0.0f;
+      }
+      act = true;
+      tag = g.snap_is_tagger[ia] != 0;
+      g.is_tagger[ia] = tag ? 1 : 0;
+      g.actions[ia * kC] = 0;
+      if (CONT) g.actions[ia * kC + 1] = 0;
+      step_count = 0;
+      if (la == 0 && L.episode != nullptr) L.episode[e] = episode;
+    }
+    if (valid && la == 0) {
+      g.step_count[e] = step_count;
+      g.done[e] = (done_now && !reset_now) ? 1 : 0;
+    }
+    // observations (write_obs_row, tag_env.cpp:165-212) of the post-step
+    // (post-reset) state; partial: the K nearest by (d2, index) over all
+    // other agents (select_k_nearest_brute, tag_env.cpp:225-237)
+    float sn = 0.f, cs = 0.f;
+    if (CONT) {
+      sn = sin_ref(dir);
+      cs = cos_ref(dir);
+    }
+    int nb[PARTIAL ? MAXK : 1];
+    if (PARTIAL) {
+      TopK<MAXK, false> top;
+      top.init(p.K);
+      for (int j = 0; j < A; ++j) {
+        const float xj = __shfl_sync(0xffffffffu, x, base + j);
+        const float yj = __shfl_sync(0xffffffffu, y, base + j);
+        if (j != la) top.consider_next(d2_of(x, y, xj, yj), j);
+      }
+#pragma unroll
+      for (int t = 0; t < (PARTIAL ? MAXK : 1); ++t) nb[t] = top.i[t];
+    }
+    float* out = stage + lane * p.D;  // this warp's staging rows: row == lane
+    const float iw = p.inv_world;
+    const int vis = PARTIAL ? p.K : A - 1;
+    for (int n = 0; n < vis; ++n) {
+      int j;
+      if (PARTIAL) {
+        j = nb[0];
+#pragma unroll
+        for (int t = 1; t < (PARTIAL ? MAXK : 1); ++t)
+          if (t == n) j = nb[t];
+      } else {
+        j = n < la ? n : n + 1;
+      }
+      // every lane of the warp joins the shuffles (j is per lane)
+      const float xj = __shfl_sync(0xffffffffu, x, base + (j < A ? j : 0));
+      const float yj = __shfl_sync(0xffffffffu, y, base + (j < A ? j : 0));
+      const bool tj = __shfl_sync(0xffffffffu, tag, base + (j < A ? j : 0));
+      const bool aj = __shfl_sync(0xffffffffu, act, base + (j < A ? j : 0));
+      float spj = 0.f, snj = 0.f, csj = 0.f;
+      if (CONT) {
+        spj = __shfl_sync(0xffffffffu, sp, base + (j < A ? j : 0));
+        snj = __shfl_sync(0xffffffffu, sn, base + (j < A ? j : 0));
+        csj = __shfl_sync(0xffffffffu, cs, base + (j < A ? j : 0));
+      }
+      if (valid) {
+        float* o = out + n * NBF;
+        if (!act) {
+#pragma unroll
+          for (int f = 0; f < NBF; ++f) st_sm(o + f, 0.0f);
+        } else {
+          st_sm(o + 0, __fmul_rn(__fsub_rn(xj, x), iw));
+          st_sm(o + 1, __fmul_rn(__fsub_rn(yj, y), iw));
+          st_sm(o + 2, tj ? 1.0f : 0.0f);
+          st_sm(o + 3, aj ? 1.0f : 0.0f);
+          if (CONT) {
+            st_sm(o + 4, __fmul_rn(spj, inv_ms(p, j)));
+            st_sm(o + 5, snj);
+            st_sm(o + 6, csj);
+          }
+        }
+      }
+    }
+    if (valid) {
+      float* o = out + vis * NBF;
+      const float tv = __fmul_rn(static_cast<float>(step_count), p.inv_episode);
+      if (!act) {
+        st_sm(o + 0, 0.0f);
+        st_sm(o + 1, 0.0f);
+        st_sm(o + 2, 0.0f);
+        if (CONT) {
+          st_sm(o + 3, 0.0f);
+          st_sm(o + 4, 0.0f);
+          st_sm(o + 5, 0.0f);
+        }
+      } else {
+        st_sm(o + 0, __fmul_rn(x, iw));
+        st_sm(o + 1, __fmul_rn(y, iw));
+        if (CONT) {
+          st_sm(o + 2, __fmul_rn(sp, inv_ms(p, la)));
+          st_sm(o + 3, sn);
+          st_sm(o + 4, cs);
+          st_sm(o + 5, tv);
+        } else {
+          st_sm(o + 2, tv);
+        }
+      }
+    }
+    // the warp's rows are one contiguous block of the obs array: coalesced
+    // streaming stores (16-byte where aligned)
+    __syncwarp();
+    {
+      const int nrows = __popc(__ballot_sync(0xffffffffu, valid));
+      const int nf = nrows * p.D;
+      const int64_t f0 = (wg * epw * A) * static_cast<int64_t>(p.D);
+      float* dst = g.obs + f0;
+      const int align = static_cast<int>((4 - (f0 & 3)) & 3);  // floats until dst is 16-B aligned
+      const int head = align < nf ? align : nf;
+      if (lane < head) __stcs(dst + lane, stage[lane]);
+      const int nv = (nf - head) >> 2;
+      const float* sv = stage + head;
+      float4* dv = reinterpret_cast<float4*>(dst + head);
+      for (int v = lane; v < nv; v += 32)
+        __stcs(dv + v, make_float4(sv[4 * v], sv[4 * v + 1], sv[4 * v + 2], sv[4 * v + 3]));
+      for (int f = head + 4 * nv + lane; f < nf; f += 32) __stcs(dst + f, stage[f]);
+    }
+    __syncwarp();
+  }
+  if (valid) {
+    g.loc_x[ia] = x;
+    g.loc_y[ia] = y;
+    if (CONT) {
+      g.speed[ia] = sp;
+      g.direction[ia] = dir;
+    }
+    g.active[ia] = act ? 1 : 0;
+  }
+  if (nonfinite && L.error) atomicOr(L.error, kErrNonFinite);
+}
+
 // ---- standalone sampler: sample_actions (sampler.cpp:5-40) ----------------
 __global__ void sample_kernel(const double* __restrict__ logits, int32_t* __restrict__ actions,
                               int64_t rows, int A, int C, int V, int64_t env_offset,
@@ -2474,8 +2786,55 @@ bool lean_plan(const TagDevConfig& p) {
          (p.A & 3) == 0 && p.bulk_in && p.lattice && p.threads_per_env == p.threads;
 }
 
+// SMALL eligibility: packed envs of at most 32 agents with full observations,
+// a fused launch with no per-env overlap flags and no rollout-capture outputs
+// (those take the main kernel). Measured against the main kernel's packed
+// path (us/step, single launch / run window): C4 2000 x 5 4.9 / 2.6 vs
+// 6.8 / 4.5, 10000 x 5 7.0 / 3.1 vs 9.8 / 5.3, continuous 2000 x 5 6.6 / 4.3
+// vs 9.1 / 6.6, A = 10 full 9.0 / 3.8 vs 11.2 / 6.3. Partial observations stay
+// on the main kernel, whose 32-bit-key brute K-NN measured faster (A = 10,
+// K = 5: 12.3 / 5.7 vs 13.2 / 8.5).
+bool small_plan(const TagDevConfig& p) {
+  return !p.use_grid && p.A <= 32 && !p.partial;
+}
+
+namespace {
+template <bool CONT, bool PARTIAL>
+cudaError_t launch_small(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L, cudaStream_t st) {
+  const int64_t epw = 32 / p.A;
+  const int64_t warps = (static_cast<int64_t>(p.E) + epw - 1) / epw;
+  const int64_t wpb = kSmallThreads / 32;
+  const unsigned blocks = static_cast<unsigned>((warps + wpb - 1) / wpb);
+  auto kern = tag_small_kernel<CONT, PARTIAL, 8>;
+  const size_t smem = static_cast<size_t>(wpb) * epw * p.A * p.D * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (err != cudaSuccess) return err;
+  }
+  if (L.pdl_wait) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p, g, L);
+  }
+  kern<<<blocks, kSmallThreads, smem, st>>>(p, g, L);
+  return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_tag_kernel(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L,
                               cudaStream_t st) {
+  if (L.mode == kModeFused && L.env_seq == nullptr && L.cap_actions == nullptr && L.cap_active == nullptr &&
+      L.cap_rewards == nullptr && L.cap_done == nullptr && small_plan(p)) {
+    return p.continuous ? launch_small<true, false>(p, g, L, st) : launch_small<false, false>(p, g, L, st);
+  }
   if (p.continuous) {
     return p.partial ? launch_g<true, true>(p, g, L, st) : launch_g<true, false>(p, g, L, st);
   }

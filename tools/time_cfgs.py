@@ -16,6 +16,8 @@ SHAPES = {
     "c2_e1776": (W.DISCRETE, 1000, 5, 1776), "c2_e2368": (W.DISCRETE, 1000, 5, 2368),
     "c2_e1184": (W.DISCRETE, 1000, 5, 1184), "c2_e4000": (W.DISCRETE, 1000, 5, 4000),
     "d100f": (W.DISCRETE, 100, 0, 2000), "c4": (W.DISCRETE, 5, 0, 2000), "d500f": (W.DISCRETE, 500, 0, 400),
+    "c4_e10000": (W.DISCRETE, 5, 0, 10000), "c4_e1": (W.DISCRETE, 5, 0, 1), "d10": (W.DISCRETE, 10, 5, 2000),
+    "d10f": (W.DISCRETE, 10, 0, 2000), "c5f": (W.CONTINUOUS, 5, 0, 2000),
 }
 for name in (sys.argv[1:] or list(SHAPES)):
     var, A, K, E = SHAPES[name]
