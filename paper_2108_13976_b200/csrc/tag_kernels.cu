@@ -2265,7 +2265,8 @@ obs_done:
 
 // ---- SMALL: warp-resident small envs (A <= 32) -----------------------------
 // RolloutDriver::step (harness.cpp:478-490) for envs of at most 32 agents
-// (C4's 1 + 4, C3's A = 10): each env is a segment of A lanes of one warp,
+// with full observations (C4's 1 + 4, C3's A = 10 full): each env is a
+// segment of A lanes of one warp,
 // one agent per lane, and the whole step runs in registers with no shared
 // memory and no barrier — neighbours' positions and flags come by
 // __shfl_sync, per-env counters by segment ballots. A launch runs n_steps
@@ -2277,7 +2278,7 @@ obs_done:
 // write_obs_row formulas, the fused reset), so results are bit-identical.
 constexpr int kSmallThreads = 64;
 
-template <bool CONT, bool PARTIAL, int MAXK>
+template <bool CONT>
 __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevConfig p, const TagDevArrays g,
                                                                   const TagLaunch L) {
   constexpr int kC = CONT ? 2 : 1;
@@ -2457,38 +2458,17 @@ __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevCo
       g.done[e] = (done_now && !reset_now) ? 1 : 0;
     }
     // observations (write_obs_row, tag_env.cpp:165-212) of the post-step
-    // (post-reset) state; partial: the K nearest by (d2, index) over all
-    // other agents (select_k_nearest_brute, tag_env.cpp:225-237)
+    // (post-reset) state: every other agent in ascending order
     float sn = 0.f, cs = 0.f;
     if (CONT) {
       sn = sin_ref(dir);
       cs = cos_ref(dir);
     }
-    int nb[PARTIAL ? MAXK : 1];
-    if (PARTIAL) {
-      TopK<MAXK, false> top;
-      top.init(p.K);
-      for (int j = 0; j < A; ++j) {
-        const float xj = __shfl_sync(0xffffffffu, x, base + j);
-        const float yj = __shfl_sync(0xffffffffu, y, base + j);
-        if (j != la) top.consider_next(d2_of(x, y, xj, yj), j);
-      }
-#pragma unroll
-      for (int t = 0; t < (PARTIAL ? MAXK : 1); ++t) nb[t] = top.i[t];
-    }
     float* out = stage + lane * p.D;  // this warp's staging rows: row == lane
     const float iw = p.inv_world;
-    const int vis = PARTIAL ? p.K : A - 1;
+    const int vis = A - 1;
     for (int n = 0; n < vis; ++n) {
-      int j;
-      if (PARTIAL) {
-        j = nb[0];
-#pragma unroll
-        for (int t = 1; t < (PARTIAL ? MAXK : 1); ++t)
-          if (t == n) j = nb[t];
-      } else {
-        j = n < la ? n : n + 1;
-      }
+      const int j = n < la ? n : n + 1;  // every other agent, ascending
       // every lane of the warp joins the shuffles (j is per lane)
       const float xj = __shfl_sync(0xffffffffu, x, base + (j < A ? j : 0));
       const float yj = __shfl_sync(0xffffffffu, y, base + (j < A ? j : 0));
@@ -2799,13 +2779,13 @@ bool small_plan(const TagDevConfig& p) {
 }
 
 namespace {
-template <bool CONT, bool PARTIAL>
+template <bool CONT>
 cudaError_t launch_small(const TagDevConfig& p, const TagDevArrays& g, const TagLaunch& L, cudaStream_t st) {
   const int64_t epw = 32 / p.A;
   const int64_t warps = (static_cast<int64_t>(p.E) + epw - 1) / epw;
   const int64_t wpb = kSmallThreads / 32;
   const unsigned blocks = static_cast<unsigned>((warps + wpb - 1) / wpb);
-  auto kern = tag_small_kernel<CONT, PARTIAL, 8>;
+  auto kern = tag_small_kernel<CONT>;
   const size_t smem = static_cast<size_t>(wpb) * epw * p.A * p.D * sizeof(float);
   if (smem > 48 * 1024) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -2833,7 +2813,7 @@ cudaError_t launch_tag_kernel(const TagDevConfig& p, const TagDevArrays& g, cons
                               cudaStream_t st) {
   if (L.mode == kModeFused && L.env_seq == nullptr && L.cap_actions == nullptr && L.cap_active == nullptr &&
       L.cap_rewards == nullptr && L.cap_done == nullptr && small_plan(p)) {
-    return p.continuous ? launch_small<true, false>(p, g, L, st) : launch_small<false, false>(p, g, L, st);
+    return p.continuous ? launch_small<true>(p, g, L, st) : launch_small<false>(p, g, L, st);
   }
   if (p.continuous) {
     return p.partial ? launch_g<true, true>(p, g, L, st) : launch_g<true, false>(p, g, L, st);

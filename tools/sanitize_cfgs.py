@@ -23,6 +23,7 @@ SHAPES = [  # (variant, taggers, runners, obs, K, grid/world, envs)
     (C, 60, 240, P, 5, 12.0, 2),   # continuous ring
     (C, 200, 800, P, 5, 20.0, 2),  # continuous ring, half-warp staging
     (C, 80, 320, P, 12, 16.0, 2),  # continuous K=12
+    (D, 2, 8, F, 5, 8, 13),        # SMALL: 3 envs per warp, partial last warp
 ]
 for var, t, r, obs, k, g, envs in SHAPES:
     kw = dict(variant=var, num_taggers=t, num_runners=r, obs_mode=obs, k_nearest=k, episode_length=4, seed=3)
@@ -40,3 +41,32 @@ for var, t, r, obs, k, g, envs in SHAPES:
     drv.check()
     print("ok", var, t + r, obs, k, ws.plan.geometry(), flush=True)
     ws.close()
+
+# the device TagReference twin (unfused sample -> run_step -> auto_reset)
+for var, t, r, obs, g in ((D, 3, 20, P, 8), (D, 20, 80, F, 10), (C, 10, 40, P, 10.0)):
+    kw = dict(variant=var, num_taggers=t, num_runners=r, obs_mode=obs, k_nearest=5, episode_length=4, seed=3)
+    kw["grid_size" if var == D else "world_length"] = g
+    cfg = W.TagConfig(**kw)
+    ws = W.Workspace(cfg, 3, reference=True)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, 1)
+    for _ in range(6):
+        drv.step()
+    ws.store.synchronize()
+    drv.check()
+    print("ok twin", var, t + r, obs, flush=True)
+    ws.close()
+
+# the pipelined host step (env-range launches) with observations
+import numpy as np  # noqa: E402
+cfg = W.TagConfig(num_taggers=20, num_runners=80, obs_mode=P, k_nearest=5, episode_length=4, seed=3)
+ws = W.Workspace(cfg, 7)
+drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, 1)
+drv.set_host_chunks(3)
+lg = np.zeros((7, 100, 1, 5))
+rw, dn, ob = np.zeros((7, 100), np.float32), np.zeros(7, np.uint8), np.zeros((7, 100, cfg.obs_dim()), np.float32)
+for _ in range(6):
+    drv.step_host(lg, lg.size, rw, dn, ob, ob.size)
+    ws.store.synchronize()
+drv.check()
+print("ok step_host", flush=True)
+ws.close()
