@@ -37,7 +37,7 @@ KEYS = [
 ]
 
 
-KERNEL = "tag_env_kernel"
+KERNEL = os.environ.get("NCU_KERNEL", "tag_env_kernel")  # e.g. NCU_KERNEL=tag_small_kernel
 
 
 def raw(rep):
