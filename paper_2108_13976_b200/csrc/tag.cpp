@@ -527,9 +527,7 @@ int TagPlan::pdl_mode() const {
 bool TagPlan::multistep_ok() {
   if (multistep_ < 0) {
     multistep_ = 1;
-    // the LEAN lattice single step (one launch per step, overlapped) beats
-    // the looped multi-step build at C2: 107 vs 117 us/step
-    if (lean_plan(dev_)) multistep_ = 0;
+
     // full observations on the grid path: the looped (multi-step) build of
     // the wide-row writer is 6-9% slower than the single-step build
     // (profiles/sweep_r01.json), which outweighs the saved state reloads
@@ -550,6 +548,9 @@ bool TagPlan::multistep_ok() {
       const double waves = ok ? static_cast<double>(dev_.grid_ctas) / (static_cast<double>(sms) * per_sm) : 0.0;
       multistep_ = waves >= 3.0 ? 1 : 0;
     }
+    // LEAN single steps (one overlapped launch per step) beat the looped
+    // multi-step build: C2 107 vs 117 us/step, continuous A = 1000 374 vs 406
+    if (lean_plan(dev_)) multistep_ = 0;
   }
   return multistep_ == 1;
 }

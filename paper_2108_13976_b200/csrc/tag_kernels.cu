@@ -1297,9 +1297,11 @@ constexpr int env_min_blocks(bool cont, int maxk) {
 // single-step one compiles the step loop away (one iteration known at compile
 // time), which keeps its code identical to a loop-free kernel — measured 35%
 // fewer instructions on the full-observation writer than the looped build.
-// LEAN: the lattice instantiation of the partial-observation step (discrete,
-// K = 5 staged rows, one env per CTA, A % 4 == 0, bulk-staged inputs, lattice
-// cells, single step, step/fused modes — launch_variant checks all of it). The
+// LEAN: the one-env instantiation of the partial-observation step (K = 5
+// staged rows, one env per CTA, A % 4 == 0, bulk-staged inputs, single step,
+// step/fused modes; discrete plans also need lattice cells — lean_plan checks
+// all of it). Continuous plans keep the ring-search K-NN and gain only the
+// compile-time layout (A = 1000: 374 vs 429 us/step). The
 // same body with those facts compile-time: the generic layouts and the
 // multi-step loop drop out (the per-agent K-NN fallback for pushed off-lattice
 // positions stays inline: an out-of-line call measured 151 vs 113 us/step, its
@@ -1312,7 +1314,8 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  static_assert(!LEAN || (!CONT && PARTIAL && GRID && EXACT && !MULTI), "LEAN is the lattice single-step case");
+  static_assert(!LEAN || (PARTIAL && GRID && EXACT && !MULTI), "LEAN is the one-env partial single step");
+  constexpr bool LATTICE_LEAN = LEAN && !CONT;
   const int tpe = LEAN ? static_cast<int>(blockDim.x) : p.threads_per_env;
   const int le = LEAN ? 0 : tid / tpe;
   const int lt = LEAN ? tid : tid - le * tpe;
@@ -1721,7 +1724,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     // Phase 2: bucket grid over post-move positions (NeighborGrid::build).
     // lattice cells are exact positions: lowest-index tagger per cell
     const bool cell_tagger = !CONT && GRID && p.lattice && all_integral && p.fault_bias == 0.0f;
-    if constexpr (LEAN) {
+    if constexpr (LATTICE_LEAN) {
       build_grid_lattice(s, p, scratch, false);
     } else {
       if (GRID && !(ablate_bits(L) & 8u)) build_grid<CONT>(s, p, scratch, false, cell_tagger);
@@ -1738,11 +1741,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       const bool runner = valid && !s.tag[a] && s.act[a];
       int best = -1;
       if (runner) {
-        if (LEAN && cell_tagger) {
+        if (LATTICE_LEAN && cell_tagger) {
           const int ct = s.celltag[s.cellof[a]];
           best = ct == 0x7fffffff ? -1 : ct;
         } else {
-          best = find_tagger<CONT, GRID>(s, p, a, cell_tagger && !LEAN, CONT ? all_integral : all_prefix);
+          best = find_tagger<CONT, GRID>(s, p, a, cell_tagger && !LATTICE_LEAN, CONT ? all_integral : all_prefix);
         }
       }
       if (best >= 0) {
@@ -1848,7 +1851,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
         }
       }
       if (PARTIAL && !CONT && GRID && p.lattice && all_integral) {
-        if constexpr (LEAN)
+        if constexpr (LATTICE_LEAN)
           build_cell_lists_keys(s, p, scratch);
         else
           build_cell_lists(s, p, ablate_bits(L));
@@ -1958,7 +1961,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   // single-env CTA: `place` is CTA-uniform here (every thread has le == 0)
   if (GRID && PARTIAL && single && place) {
     __syncthreads();
-    if constexpr (LEAN)
+    if constexpr (LATTICE_LEAN)
       build_grid_lattice(s, p, scratch, true);
     else
       build_grid<CONT>(s, p, scratch, true);
@@ -1986,7 +1989,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     const bool cell_lists = PARTIAL && lattice_ok;  // GRID => single env per CTA
     const int kk = p.K + 1;
     if (cell_lists && !early_inputs) {
-      if constexpr (LEAN)
+      if constexpr (LATTICE_LEAN)
         build_cell_lists_keys(s, p, scratch);
       else
         build_cell_lists(s, p, ablate_bits(L));
@@ -2698,8 +2701,8 @@ cudaError_t launch_variant(const TagDevConfig& p, const TagDevArrays& g, const T
   // 6-35% slower there.
   auto kern = (L.n_steps > 1 || PARTIAL) ? tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, true>
                                          : tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, false>;
-  if constexpr (!CONT && PARTIAL && GRID && EXACT) {
-    // the lattice single step (see LEAN at tag_env_kernel)
+  if constexpr (PARTIAL && GRID && EXACT) {
+    // the one-env single step (see LEAN at tag_env_kernel)
     const bool lean = L.mode >= 0 && L.mode != kModeReinit && L.n_steps <= 1 && lean_plan(p);
     if (lean) kern = tag_env_kernel<CONT, PARTIAL, GRID, MAXK, EXACT, false, true>;
   }
@@ -2762,8 +2765,8 @@ cudaError_t launch_g(const TagDevConfig& p, const TagDevArrays& g, const TagLaun
 
 // ---- host-callable launchers (declared in kernels.hpp) ---------------------
 bool lean_plan(const TagDevConfig& p) {
-  return !p.continuous && p.partial && p.use_grid && p.K == 5 && p.stage_obs && p.envs_per_cta == 1 &&
-         (p.A & 3) == 0 && p.bulk_in && p.lattice && p.threads_per_env == p.threads;
+  return p.partial && p.use_grid && p.K == 5 && p.stage_obs && p.envs_per_cta == 1 && (p.A & 3) == 0 &&
+         p.bulk_in && p.threads_per_env == p.threads && (p.continuous || p.lattice);
 }
 
 // SMALL eligibility: packed envs of at most 32 agents with full observations,
