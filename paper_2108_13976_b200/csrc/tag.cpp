@@ -158,7 +158,8 @@ int resident_ctas(const TagDevConfig& p) {
 // register cap already holds it at 3, 265 -> 285 us/step.
 TagDevConfig make_dev_config(const DataStore& store, const wdg_tag_config& cfg) {
   TagDevConfig full = make_dev_config_rows(store, cfg, 32);
-  if (!full.continuous || !full.partial || full.K != 5 || !full.use_grid || !full.stage_obs) return full;
+  if (full.fallback || !full.continuous || !full.partial || full.K != 5 || !full.use_grid || !full.stage_obs)
+    return full;
   const int64_t forced = tuning("stage_rows", 0);
   if (forced == 32) return full;
   TagDevConfig half = make_dev_config_rows(store, cfg, 16);
@@ -174,8 +175,8 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   if (store.num_agents() != A) {
     raise(Errc::shape_mismatch, "tag plan: store num_agents != config agents");
   }
-  if (A > 65535) raise(Errc::invalid_config, "device Tag path supports at most 65535 agents per env");
   if (store.num_envs() > (int64_t{1} << 31) - 1) raise(Errc::invalid_config, "too many envs");
+  if (A > 65535) p.fallback = 1;  // 16-bit agent indices in the shared-memory tables
   p.E = static_cast<int32_t>(store.num_envs());
   p.A = static_cast<int32_t>(A);
   p.T = static_cast<int32_t>(cfg.num_taggers);
@@ -184,9 +185,7 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   p.C = p.continuous ? 2 : 1;
   p.V = p.continuous ? 3 : 5;
   p.K = p.partial ? static_cast<int32_t>(cfg.k_nearest) : 0;
-  if (p.partial && p.K > 32) {
-    raise(Errc::invalid_config, "device Tag path supports k_nearest <= 32");
-  }
+  if (p.partial && p.K > 32) p.fallback = 1;  // register top-K lists
   p.vis = p.partial ? p.K : p.A - 1;
   p.D = static_cast<int32_t>(tag_obs_dim(cfg));
   p.env_offset = store.env_offset();
@@ -210,6 +209,8 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   p.inv_max_speed_runner = 1.0f / p.max_speed_runner;
   p.fault_bias = fault_tag_radius_bias();
   p.placement_h0 = host_mix64(host_substream(cfg.seed, kStreamPlacement));
+
+  if (p.fallback) return p;  // the global-memory kernels need no geometry
 
   // Geometry: grid path = one env per CTA; brute path packs envs per CTA.
   // Discrete lattice cells (one bucket per grid point) once the grid is at
@@ -368,10 +369,10 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
       p.prefetch_stride = static_cast<int32_t>(tuning("l2_prefetch", 0));
     }
   }
-  if (total > kMaxSmem) {
-    raise(Errc::invalid_config, "device Tag path: " + std::to_string(A) +
-                                    " agents need " + std::to_string(total) +
-                                    " B of shared memory per env (max 227 KB)");
+  if (total > kMaxSmem) {  // too large for one CTA's shared memory
+    TagDevConfig f = p;
+    f.fallback = 1;
+    return f;
   }
   p.smem_bytes = static_cast<int32_t>(total);
   return p;
@@ -459,10 +460,25 @@ void register_tag_arrays(DataStore& store, const wdg_tag_config& cfg) {
   // with episode 0 on every env), then captured as the registration snapshot.
   TagDevConfig p = make_dev_config(store, cfg);
   TagDevArrays g = bind_dev_arrays(store, cfg);
-  TagLaunch L;
-  L.mode = kModeReinit;
-  L.init_episode = 1;
-  cuda_check(launch_tag_kernel(p, g, L, store.stream()), "register_tag_arrays init kernel");
+  if (p.fallback) {  // episode-0 placement + observations by the global-memory kernels
+    float* kd = nullptr;
+    int32_t* ki = nullptr;
+    if (p.partial) {
+      const size_t n = static_cast<size_t>(p.E) * p.A * p.K;
+      cuda_check(cudaMalloc(&kd, n * sizeof(float)), "cudaMalloc(knn scratch)");
+      cuda_check(cudaMalloc(&ki, n * sizeof(int32_t)), "cudaMalloc(knn scratch)");
+    }
+    const cudaError_t err = launch_twin_kernel(p, g, kModeReinit, nullptr, nullptr, kd, ki, store.stream());
+    if (err == cudaSuccess) cudaStreamSynchronize(store.stream());
+    if (kd) cudaFree(kd);
+    if (ki) cudaFree(ki);
+    cuda_check(err, "register_tag_arrays init kernel (global-memory path)");
+  } else {
+    TagLaunch L;
+    L.mode = kModeReinit;
+    L.init_episode = 1;
+    cuda_check(launch_tag_kernel(p, g, L, store.stream()), "register_tag_arrays init kernel");
+  }
   for (const char* n : {"loc_x", "loc_y", "speed", "direction", "active"}) {
     if (store.has_array(n)) store.refresh_snapshot(store.handle(n));
   }
@@ -476,6 +492,10 @@ TagPlan::TagPlan(DataStore& store, const wdg_tag_config& cfg, bool reference)
   if (!store.locked()) raise(Errc::state_error, "build_tag_plan: store must be locked");
   dev_ = make_dev_config(store, cfg);
   arrays_ = bind_dev_arrays(store, cfg);
+  // A shape the shared-memory kernels cannot take steps on the global-memory
+  // kernels (the same code as the check's TagReference twin, parity-tested),
+  // through the unfused sample -> run_step -> auto_reset sequence.
+  if (dev_.fallback) reference_ = true;
   if (reference_) {
     if (dev_.partial) {
       const size_t n = static_cast<size_t>(dev_.E) * dev_.A * dev_.K;

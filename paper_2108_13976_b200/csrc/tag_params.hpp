@@ -98,6 +98,10 @@ struct TagDevConfig {
   int32_t off_zone = 0;           // CTA offset of the bulk logits landing zone
   int32_t prefetch_stride = 0;    // bulk path: L2-prefetch env e + stride's inputs (0 = off)
   int32_t smem_bytes = 0;         // total dynamic smem per CTA
+  // Shapes the shared-memory kernels cannot take (k_nearest > 32, more than
+  // 65535 agents, or more than 227 KB of shared memory per env) run on the
+  // global-memory TagReference kernels (twin_kernels.cu) instead.
+  int32_t fallback = 0;
 };
 
 // Per-launch arguments.

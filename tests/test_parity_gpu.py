@@ -500,11 +500,35 @@ def test_fault_injection_detected_in_rewards():
         W.set_fault_tag_radius_bias(0.0)
 
 
-def test_unsupported_shapes_fail_loudly():
-    with pytest.raises(W.WarpError) as ei:
-        dc, _ = cfg_pair(num_taggers=10, num_runners=40, obs_mode=O.PARTIAL, k_nearest=40)
-        W.Workspace(dc, 2)
-    assert ei.value.code == W.INVALID_CONFIG
+@pytest.mark.parametrize("kw,envs,steps", [
+    # k_nearest > 32 (the shared-memory kernels keep top-K lists in registers)
+    (dict(num_taggers=10, num_runners=40, obs_mode=O.PARTIAL, k_nearest=40, episode_length=6, seed=3), 3, 10),
+    (dict(variant=O.CONTINUOUS, num_taggers=8, num_runners=40, obs_mode=O.PARTIAL, k_nearest=33,
+          episode_length=6, world_length=6.0, tag_radius=0.8, seed=4), 2, 8),
+    # more than 227 KB of shared memory per env
+    (dict(num_taggers=2400, num_runners=9600, obs_mode=O.PARTIAL, episode_length=3, seed=5), 1, 4),
+])
+def test_large_shapes_run_on_the_global_memory_path(kw, envs, steps):
+    """Shapes the shared-memory kernels cannot take (k_nearest > 32, more
+    than 65535 agents, more than 227 KB of shared memory per env) run on the
+    global-memory kernels (the TagReference twin's code) instead of failing;
+    the reference only requires k < agents (tag_env.cpp:36-39). Bit-exact
+    against the oracle through the fused-looking driver (unfused underneath)."""
+    if kw.get("variant") == O.CONTINUOUS and not O.libm_matches_replica():
+        pytest.skip("host libm is not the glibc FMA variant the device replicates")
+    dc, oc = cfg_pair(**kw)
+    ws = W.Workspace(dc, envs)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, oc.seed)
+    o = O.OracleWorld(oc, envs)
+    assert_same(dev_snapshot(ws, o.layout), o.snapshot(), "registration")
+    for t in range(steps):
+        drv.step()
+        o.rollout(t, 1, oc.seed)
+        assert_same(dev_snapshot(ws, o.layout), o.snapshot(), f"step {t}")
+    drv.check()
+    for e in range(envs):
+        assert ws.resets.episodes_started(e) == o.episodes(e)
+    ws.close()
 
 
 def test_cpp_facade_example(tmp_path):
