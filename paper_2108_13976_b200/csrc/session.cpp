@@ -5,6 +5,9 @@
 // bench-agents (harness.cpp:563-898) driving the B200 kernels. Training is the
 // reference's CPU learner and stays out of scope.
 //
+// parse_config / config_to_json follow harness.cpp:92-206 key by key (copied
+// for byte-identical output, see StrictObj below).
+//
 // Compiled by nvcc (-x cu): the store comparison of `check` is a device kernel
 // (compare_stores, harness.cpp:531-557, without pulling the stores to host).
 #include <cuda_runtime.h>
@@ -83,7 +86,11 @@ struct RunConfig {
   RunSettings run;
 };
 
-// StrictObj (harness.cpp:32-66): unknown keys and type errors are parse errors.
+// StrictObj: copied from the reference (harness.cpp:32-66) with its key lists
+// and error strings, because the canonical JSON, the FNV-1a config hash and the
+// parse-error text must be byte-identical to the reference's (schema
+// conformance, tests/test_session.py). Unknown keys and type errors are parse
+// errors.
 class StrictObj {
  public:
   StrictObj(const json& j, std::string path) : j_(j), path_(std::move(path)) {
