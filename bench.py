@@ -203,6 +203,47 @@ def run_reference(args, rank, world):
     return 0
 
 
+# ---- BASELINE configs[2..3] points measured in the same run (informational) ---------
+def sweep_points(W, torch, stream, steps):
+    """C3 agent sweep (2000 envs, partial K=5, T = llround(A/5)), C4 env sweep
+    (1 + 4 agents, full obs) and continuous A = 1000, device-timed like `value`
+    (one fused launch per step, or RolloutDriver::run windows for C4)."""
+    def time_steps(cfg, E, n, run):
+        ws = W.Workspace(cfg, E, stream=stream)
+        drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, cfg.seed)
+        for _ in range(3):
+            drv.step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if run:
+            drv.run(n)
+        else:
+            for _ in range(n):
+                drv.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        drv.check()
+        ws.close()
+        return e0.elapsed_time(e1) * 1e3 / n  # us per step
+    out = {"note": "informational; `value` is C2 only", "c3_partial_2000_envs": {}, "c4_1plus4_full": {}}
+    for A in (10, 100, 500):
+        T = int(A / 5 + 0.5)
+        cfg = W.TagConfig(num_taggers=T, num_runners=A - T, obs_mode=W.PARTIAL, k_nearest=5)
+        us = time_steps(cfg, 2000, steps, False)
+        out["c3_partial_2000_envs"][str(A)] = {"us_per_step": us, "env_steps_per_s": 2000 / us * 1e6}
+    for E in (1, 100, 2000, 10000):
+        cfg = W.TagConfig(num_taggers=1, num_runners=4)
+        single = time_steps(cfg, E, steps, False)
+        run = time_steps(cfg, E, 64 * max(1, steps // 64), True)
+        out["c4_1plus4_full"][str(E)] = {"single_launch_us_per_step": single, "run_us_per_step": run,
+                                         "env_steps_per_s_run": E / run * 1e6}
+    cfg = W.TagConfig(variant=W.CONTINUOUS, num_taggers=200, num_runners=800, obs_mode=W.PARTIAL, k_nearest=5)
+    us = time_steps(cfg, 2000, max(20, steps // 4), False)
+    out["continuous_partial_2000x1000"] = {"us_per_step": us, "env_steps_per_s": 2000 / us * 1e6}
+    return out
+
+
 # ---- our arm ---------------------------------------------------------------------
 def reference_engine_sample(threads, envs=256, steps=20, timeout=180):
     """CPU variant (i), reference-faithful: ONE reference world whose
@@ -458,6 +499,12 @@ def run_ours(args, rank, world, local_rank):
     e2e_open["path"] = "wdg_rollout_step_host, open loop (no host wait between steps)"
     drv.check()
     clocks.stop()
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        try:
+            sweep = sweep_points(W, torch, stream, 128)
+        except Exception as exc:  # reported, never required
+            sweep = {"error": str(exc)}
 
     if rank == 0:
         peak, peak_kind = measured_peak_hbm()
@@ -497,6 +544,8 @@ def run_ours(args, rank, world, local_rank):
             "episode_stats": {"episodes": stats[0], "tag_events": stats[3], "env_steps": stats[4]},
             "clocks": clocks.summary(),
         }
+        if sweep is not None:
+            line["sweep"] = sweep
         if world > 1:
             collective["allreduces_timed"] = allreduces
             collective["stats_every"] = stats_every
@@ -521,6 +570,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=400)  # ~10 s of reference CPU work over 2000 envs
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-engine-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     # Test-only: run every rank on cuda:0 over gloo, to exercise the N>1
     # logic (shards, barriers, max-over-ranks, stats all-reduce) on one GPU.
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)

@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TA
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 20 --warmup 3 --e2e-steps 2 --no-cpu-baseline > /dev/null 2>&1
+  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 20 --warmup 3 --e2e-steps 2 --no-cpu-baseline --no-sweep > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tag_env_kernel -s 6 -c 1 \
   -o gpurun_out/${TAG}_prof_c2 python tools/profile_c2.py 8 > gpurun_out/${TAG}_ncu_full.log 2>&1
 if [ "$2" == "sweep" ]; then
