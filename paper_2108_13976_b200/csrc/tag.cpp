@@ -234,16 +234,17 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   p.use_grid = A > brute_max ? 1 : 0;
   if (p.use_grid) {
     // One env per CTA, one thread per agent up to the CTA cap (larger A
-    // loops). WDG_TPE_MAX overrides the cap (tuning experiments).
-    // Thread cap per env, measured at 2000 envs, partial K=5 (us/step at
-    // 128 / 192 / 256 threads): discrete A = 200 85 / - / 97, 300 86 / - / 102,
-    // 500 89 / - / 104, 700 130 / 112 / 118, 1000 177 / 160 / 136;
-    // continuous A = 300 201 / 218 / 250, 500 298 / 277 / 280, 1000 600 / - / 476.
-    // Smaller envs keep more CTAs (envs) per SM overlapping each other's
-    // barriers; at C2 four 256-thread envs per SM are best.
+    // loops). Thread cap per env, re-measured in round 2 on the LEAN kernels
+    // at 2000 envs, partial K=5 (us/step at 128 / 192 / 256 threads,
+    // tools/tune_scan.py): discrete A = 200 56 / 71 / 83, 300 63 / 74 / 76,
+    // 400 71 / 80 / 76, 500 86 / 83 / 78, 700 108 / 94 / 88, 864 - / 120 / 95;
+    // continuous A = 300 166 / 176 / 204, 400 188 / 196 / 217, 500 246 / 211 /
+    // 224, 600 263 / 240 / 260, 700 - / 292 / 270, 800 - / 342 / 290,
+    // 1000 477 / 393 / 360. Smaller envs keep more CTAs (envs) per SM
+    // overlapping each other's barriers; larger ones gain from wider CTAs.
     int cap = 256;
-    if (p.partial && (p.continuous ? A <= 400 : A <= 512)) cap = 128;
-    else if (p.partial && !p.continuous && A <= 864) cap = 192;
+    if (p.partial && (p.continuous ? A <= 400 : A <= 448)) cap = 128;
+    else if (p.partial && p.continuous && A <= 650) cap = 192;
     if (const int64_t t = tuning("threads_per_env_max", 0)) cap = static_cast<int>(std::clamp<int64_t>(t, 32, 1024)) / 32 * 32;
     cap = std::min(cap, kMaxThreadsPerCta);
     p.envs_per_cta = 1;
@@ -540,7 +541,12 @@ void TagPlan::launch(TagLaunch L) {
 int TagPlan::pdl_mode() const {
   if (const int64_t t = tuning("pdl_mode", -1); t >= 0) return static_cast<int>(t);  // A/B experiments, tests
   if (!dev_.use_grid) return (dev_.envs_per_cta <= 4 && dev_.threads >= 128) ? 1 : 3;
-  if (!dev_.continuous && dev_.partial && dev_.threads < 256) return 2;
+  // Grid plans: released at CTA entry. Re-measured in round 2 on the LEAN
+  // kernels (us/step, modes 0 / 1 / 2 / 3): discrete A = 200 (128 threads)
+  // 57 / 50 / 57 / 56, A = 400 72 / 65 / 71 / 70, A = 500 87 / 78 / 89 / 85,
+  // C2 112 / 99 / 114 / 110; continuous A = 300 188 / 166 / 174 / 186, A = 500
+  // 254 / 211 / 238 / 252 (round 1's exit release for small discrete grids no
+  // longer pays).
   return 1;
 }
 
