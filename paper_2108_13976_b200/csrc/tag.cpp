@@ -132,7 +132,7 @@ namespace {
 constexpr int kNumSMs = 148;
 constexpr int kBruteMaxAgents = 64;    // brute-force K-NN/resolve up to this (full obs)
 constexpr int kBruteMaxPartialDisc = 192;  // ... partial obs, discrete without lattice cells
-constexpr int kBruteMaxPartialCont = 256;  // ... partial obs, continuous
+constexpr int kBruteMaxPartialCont = 200;  // ... partial obs, continuous
 constexpr int kMaxSmem = 227 * 1024;
 
 int32_t round_up(int64_t v, int64_t m) { return static_cast<int32_t>((v + m - 1) / m * m); }
@@ -220,10 +220,14 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   // A = 100 it loses (99 vs 76, gc 10).
   const int64_t g = cfg.grid_size;
   const int64_t lattice_cell_bytes = 9 + (p.partial ? 4 * (int64_t{p.K} + 1) : 0);
-  const bool lattice_fits = !p.continuous && g <= 128 && g * g <= 2 * A &&
+  // Round 2 (LEAN lattice kernel, 2000 envs, grid 20, us/step lattice vs
+  // brute): A = 150 87 vs 60, A = 192 50 vs 75 -> lattice from 0.4 agents per cell.
+  const bool lattice_fits = !p.continuous && g <= 128 && 2 * g * g <= 5 * A &&
                             g * g * lattice_cell_bytes <= 96 * 1024;
   // Partial obs keeps the brute-force K-NN (one env per <= 8 warps) where it
-  // beats the bucket grid at 2000 envs, K=5 (us/step, brute vs grid):
+  // beats the bucket grid at 2000 envs, K=5 (us/step, brute vs grid; round 2
+  // on the LEAN grid kernels: continuous A = 100 57 vs 100, 200 141 vs 142,
+  // 256 178 vs 146 -> brute up to 200):
   // discrete A = 100 41 vs 76, 160 63 vs 140 (ring), 256 121 vs 99 (lattice);
   // continuous A = 100 63 vs 103, 200 148 vs 192, 256 185 vs 196.
   int brute_max = !p.partial ? kBruteMaxAgents

@@ -32,16 +32,19 @@ def time_shape(var, A, K, E, steps=100):
 
 
 SCANS = [
-    ("disc200", (W.DISCRETE, 200, 5, 2000), "pdl_mode", [0, 1, 2, 3]),
-    ("disc400", (W.DISCRETE, 400, 5, 2000), "pdl_mode", [0, 1, 2, 3]),
-    ("disc500", (W.DISCRETE, 500, 5, 2000), "pdl_mode", [0, 1, 2, 3]),
-    ("cont300", (W.CONTINUOUS, 300, 5, 2000), "pdl_mode", [0, 1, 2, 3]),
-    ("cont500", (W.CONTINUOUS, 500, 5, 2000), "pdl_mode", [0, 1, 2, 3]),
-    ("disc1000", (W.DISCRETE, 1000, 5, 2000), "pdl_mode", [0, 1, 2, 3]),
+    ("disc160", (W.DISCRETE, 160, 5, 2000), "combo", [None, {"brute_max": 256}]),
+    ("disc176", (W.DISCRETE, 176, 5, 2000), "combo", [None, {"brute_max": 256}]),
+    ("disc192", (W.DISCRETE, 192, 5, 2000), "combo", [None]),
+    ("cont200", (W.CONTINUOUS, 200, 5, 2000), "combo", [None]),
+    ("cont240", (W.CONTINUOUS, 240, 5, 2000), "combo", [None, {"brute_max": 256}]),
 ]
 for name, shape, key, vals in SCANS:
     for v in vals:
-        W.set_tuning(key, v)
+        if key == "combo":
+            for k2, v2 in (v or {}).items():
+                W.set_tuning(k2, v2)
+        else:
+            W.set_tuning(key, v)
         try:
             us, geo = time_shape(*shape)
             print(f"{name} {key}={v}: {us:.1f} us/step  threads={geo['threads_per_cta']} smem={geo['smem_bytes']}",
