@@ -1,7 +1,7 @@
 """Per-kernel counts of the SASS mnemonics that show which hardware paths the
 built kernels use (TMA bulk copies, mbarriers, tcgen05 MMA / TMEM, streaming
 stores), from `cuobjdump -sass` of the in-tree objects. Writes
-profiles/sass_r01.md.   python tools/sass_evidence.py"""
+profiles/sass_r02.md.   python tools/sass_evidence.py"""
 import collections
 import os
 import re
@@ -10,7 +10,7 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_2108_13976_b200", "lib", "obj")
 KEYS = ["UBLKCP", "SYNCS.ARRIVE", "SYNCS.PHASECHK", "UTCHMMA", "UTCBAR", "LDTM", "MUFU.TANH", "MUFU.EX2",
-        "STG.E.EF", "BAR.SYNC", "DFMA", "HMMA"]
+        "STG.E.EF", "BAR.SYNC", "SHFL", "DFMA", "HMMA"]
 
 
 def demangle(names):
@@ -20,7 +20,7 @@ def demangle(names):
 
 def main():
     rows = []
-    for obj in ("tag_kernels.o", "policy.o", "batch.o"):
+    for obj in ("tag_kernels.o", "twin_kernels.o", "policy.o", "batch.o"):
         sass = subprocess.run(["cuobjdump", "-sass", os.path.join(OBJ, obj)], capture_output=True, text=True).stdout
         cur, counts = None, collections.OrderedDict()
         for ln in sass.splitlines():
@@ -42,7 +42,7 @@ def main():
                 continue
             short = re.sub(r"\(.*", "", d.replace("wdg::(anonymous namespace)::", ""))
             rows.append((obj, short, counts[n]))
-    lines = ["# SASS evidence (round 1)", "",
+    lines = ["# SASS evidence (round 2)", "",
              "`cuobjdump -sass` of the in-tree sm_100a objects, by `tools/sass_evidence.py`. Counts are static",
              "instructions per kernel. `UBLKCP` = `cp.async.bulk` global->shared (the Tag kernel's input",
              "staging); `SYNCS.*` = mbarrier arrive / try-wait; `UTCHMMA` / `UTCBAR` / `LDTM` = tcgen05 MMA,",
@@ -50,7 +50,7 @@ def main():
              "| object | kernel | " + " | ".join(KEYS) + " |", "|---|---|" + "---|" * len(KEYS)]
     for obj, k, c in rows:
         lines.append(f"| {obj} | `{k}` | " + " | ".join(str(c.get(x, 0)) for x in KEYS) + " |")
-    open(os.path.join(ROOT, "profiles", "sass_r01.md"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(ROOT, "profiles", "sass_r02.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines[:12]), f"\n... {len(rows)} kernels")
 
 
