@@ -374,7 +374,9 @@ __global__ void __launch_bounds__(kBfThreads, WDG_BF16_MIN_BLOCKS) policy_bf16_k
   // registers one tile ahead so the global latency overlaps the MMA chain.
   const bool small = rows < (int64_t{1} << 31);
   auto row_of = [&](int64_t tile, int64_t& e, int64_t& ag) {
-    const int64_t r = tile * kBfRows + tid;
+    // tiles from the end: the step kernel wrote the last envs' observations
+    // last, so their lines are the ones still in L2
+    const int64_t r = (tiles - 1 - tile) * kBfRows + tid;
     const bool ok = r < rows;
     if (small) {  // 32-bit division (the common case)
       const uint32_t r32 = ok ? static_cast<uint32_t>(r) : 0u, n32 = static_cast<uint32_t>(a.n);
