@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <numeric>
 #include <set>
 
 #include "facade.hpp"
@@ -592,6 +593,9 @@ void TagPlan::launch_envs(TagLaunch L, int64_t e0, int64_t n) {
   if (e0 == 0 && n == dev_.E) return launch(L);
   if (reference_) raise(Errc::state_error, "tag plan: the TagReference twin runs run_step / reinit only");
   if (e0 < 0 || n <= 0 || e0 + n > dev_.E) raise(Errc::index_out_of_range, "tag launch: env range");
+  if ((e0 * dev_.A * dev_.D) % 4 != 0 || (e0 * dev_.A) % 4 != 0) {
+    raise(Errc::invalid_argument, "tag launch: env range must start on 16-byte boundaries of the arrays");
+  }
   TagDevConfig d = dev_;
   d.fault_bias = fault_tag_radius_bias();
   d.E = static_cast<int32_t>(n);
@@ -1136,9 +1140,14 @@ void Rollout::step_host(const double* host_logits, int64_t count, float* host_re
   int chunks = host_chunks_ > 0 ? host_chunks_
                                 : static_cast<int>(std::clamp<int64_t>(static_cast<int64_t>(bytes >> 23), 1, kMaxHostChunks));
   if (!fused) chunks = 1;
-  const int64_t epc = p.envs_per_cta;
+  // chunk boundaries on whole CTAs and on 16-byte boundaries of the
+  // observation rows (the kernels store them as 16-byte vectors from the
+  // chunk's first row): e0 * A * D % 4 == 0
+  const int64_t row_floats = int64_t{p.A} * p.D;
+  const int64_t align = std::lcm<int64_t>(4 / std::gcd<int64_t>(row_floats, 4), 4 / std::gcd<int64_t>(p.A, 4));
+  const int64_t unit = std::lcm<int64_t>(p.envs_per_cta, align);
   const int64_t per = (int64_t{p.E} + chunks - 1) / chunks;
-  const int64_t per_chunk = std::max<int64_t>(epc, (per + epc - 1) / epc * epc);
+  const int64_t per_chunk = std::max<int64_t>(unit, (per + unit - 1) / unit * unit);
   const int slot = static_cast<int>(t_ & 1);
   cudaStream_t st = store_.stream();
   // The slot was last read by the kernels of step t-2.

@@ -45,6 +45,11 @@ HOST_CASES = {
                                  seed=17), 40),
     # full observations, packed envs (several envs per CTA)
     "disc_full_30x20": (dict(num_taggers=4, num_runners=16, episode_length=10, grid_size=6, seed=8), 30),
+    # C4's 1 + 4 agents: 95-float rows, so chunk starts must keep 16-byte alignment
+    "disc_full_43x5": (dict(num_taggers=1, num_runners=4, episode_length=7, grid_size=4, seed=9), 43),
+    # continuous partial on the one-env grid path
+    "cont_partial_12x300": (dict(variant=O.CONTINUOUS, num_taggers=60, num_runners=240, obs_mode=O.PARTIAL,
+                                 episode_length=8, world_length=12.0, tag_radius=0.6, seed=10), 12),
 }
 
 
@@ -53,9 +58,11 @@ HOST_CASES = {
 @pytest.mark.parametrize("with_obs", [True, False])
 def test_step_host_matches_oracle(name, mode, with_obs):
     kw, E = HOST_CASES[name]
+    if kw.get("variant") == O.CONTINUOUS and not O.libm_matches_replica():
+        pytest.skip("host libm is not the glibc FMA variant the device replicates")
     dc, oc = cfg_pair(**kw)
     A = oc.num_taggers + oc.num_runners
-    C, V, D = 1, 5, dc.obs_dim()
+    C, V, D = dc.action_categories(), dc.action_choices(), dc.obs_dim()
     ws = W.Workspace(dc, E)
     drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, kw["seed"])
     if mode == "unfused":
