@@ -56,6 +56,8 @@ enum class ElementKind : int32_t { Real32 = WDG_REAL32, Int32 = WDG_INT32, Bool8
 enum class TagVariant : int32_t { Discrete = WDG_TAG_DISCRETE, Continuous = WDG_TAG_CONTINUOUS };
 enum class ObsMode : int32_t { Full = WDG_OBS_FULL, Partial = WDG_OBS_PARTIAL };
 
+inline constexpr const char* kLocX = "loc_x";
+inline constexpr const char* kLocY = "loc_y";
 inline constexpr const char* kObservations = "observations";
 inline constexpr const char* kSampledActions = "sampled_actions";
 inline constexpr const char* kRewards = "rewards";
@@ -175,6 +177,12 @@ inline std::vector<std::string> tag_zero_on_reset() {
 class TagPlan {
  public:
   TagPlan(DataStore& store, const TagConfig& cfg) { check(wdg_build_tag_plan(store.raw(), &cfg, &h_)); }
+  // TagReference(store, cfg) (tag_env.cpp:505-595): the device twin, the
+  // consistency check's independent second implementation.
+  struct Reference {};
+  TagPlan(DataStore& store, const TagConfig& cfg, Reference) {
+    check(wdg_build_tag_reference(store.raw(), &cfg, &h_));
+  }
   ~TagPlan() { wdg_tag_plan_destroy(h_); }
   TagPlan(const TagPlan&) = delete;
   TagPlan& operator=(const TagPlan&) = delete;
@@ -290,6 +298,7 @@ class RolloutDriver {
   ~RolloutDriver() { wdg_rollout_destroy(h_); }
   RolloutDriver(const RolloutDriver&) = delete;
   RolloutDriver& operator=(const RolloutDriver&) = delete;
+  wdg_rollout* raw() const { return h_; }
   void set_logits(const double* device_logits, int64_t count) {
     check(wdg_rollout_set_logits(h_, device_logits, count));
   }
@@ -308,6 +317,8 @@ class RolloutDriver {
     check(wdg_rollout_step_host_obs(h_, host_logits, count, host_rewards, host_done, host_obs, obs_count));
   }
   void set_host_chunks(int32_t chunks) { check(wdg_rollout_set_host_chunks(h_, chunks)); }
+  // overlapped consecutive launches (default on); false = serial launches
+  void set_overlap(bool enabled) { check(wdg_rollout_set_overlap(h_, enabled ? 1 : 0)); }
   void run(int64_t steps) { check(wdg_rollout_run(h_, steps)); }
   void check_errors() { check(wdg_rollout_check(h_)); }
   std::vector<double> stats() {
@@ -318,6 +329,35 @@ class RolloutDriver {
 
  private:
   wdg_rollout* h_ = nullptr;
+};
+
+// Plan tuning overrides (wdg_set_tuning): how a plan maps the step onto the
+// GPU, never what it computes; value < 0 restores the plan's choice.
+inline void set_tuning(const std::string& key, int64_t value) { check(wdg_set_tuning(key.c_str(), value)); }
+
+// The episode-statistics all-reduce of a sharded run:
+// rank 0 creates the id, every rank builds the communicator from it.
+class Comm {
+ public:
+  static std::vector<uint8_t> unique_id() {
+    std::vector<uint8_t> id(128);
+    check(wdg_comm_unique_id(id.data(), static_cast<int64_t>(id.size())));
+    return id;
+  }
+  Comm(int32_t world, int32_t rank, const std::vector<uint8_t>& id) {
+    check(wdg_comm_init(world, rank, id.data(), static_cast<int64_t>(id.size()), &h_));
+  }
+  explicit Comm(void* nccl_comm) { check(wdg_comm_wrap(nccl_comm, &h_)); }  // not owned
+  ~Comm() { wdg_comm_destroy(h_); }
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  // tracker sums of this shard -> ncclAllReduce(sum) into device double[8]
+  void stats_allreduce(RolloutDriver& rollout, double* device_out) {
+    check(wdg_stats_allreduce(rollout.raw(), h_, device_out));
+  }
+
+ private:
+  wdg_comm* h_ = nullptr;
 };
 
 }  // namespace warp_b200

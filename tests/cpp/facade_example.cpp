@@ -37,7 +37,29 @@ int main() {
     driver.check_errors();
     const std::vector<double> st2 = driver.stats();
     std::printf("policy rollout: env_steps=%.0f\n", st2[WDG_STAT_ENV_STEPS]);
-    return (st[WDG_STAT_ENV_STEPS] == 16 * 40 && st2[WDG_STAT_ENV_STEPS] == 16 * 50) ? 0 : 1;
+    // The TagReference twin (tag_env.cpp:505-595) on its own store, stepped
+    // with serial launches: same seeds -> the same positions as the fused plan.
+    DataStore ref_store(16, cfg.num_agents());
+    register_tag_arrays(ref_store, cfg);
+    ref_store.lock();
+    TagPlan twin(ref_store, cfg, TagPlan::Reference{});
+    ResetManager ref_resets(ref_store, true, tag_zero_on_reset(), &twin);
+    RolloutDriver ref_driver(ref_store, twin, &ref_resets, cfg.seed);
+    ref_driver.set_overlap(false);
+    DataStore cmp_store(16, cfg.num_agents());
+    register_tag_arrays(cmp_store, cfg);
+    cmp_store.lock();
+    TagPlan fused(cmp_store, cfg);
+    ResetManager cmp_resets(cmp_store, true, tag_zero_on_reset(), &fused);
+    RolloutDriver cmp_driver(cmp_store, fused, &cmp_resets, cfg.seed);
+    ref_driver.run(30);
+    cmp_driver.run(30);
+    ref_driver.check_errors();
+    cmp_driver.check_errors();
+    const bool twin_equal = ref_store.pull<int32_t>(kLocX) == cmp_store.pull<int32_t>(kLocX) &&
+                            ref_store.pull<float>(kObservations) == cmp_store.pull<float>(kObservations);
+    std::printf("twin vs fused after 30 steps: %s\n", twin_equal ? "equal" : "DIFFERENT");
+    return (st[WDG_STAT_ENV_STEPS] == 16 * 40 && st2[WDG_STAT_ENV_STEPS] == 16 * 50 && twin_equal) ? 0 : 1;
   } catch (const Error& e) {
     std::fprintf(stderr, "error %d: %s\n", static_cast<int>(e.code()), e.what());
     return 2;
