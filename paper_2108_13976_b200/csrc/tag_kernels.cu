@@ -60,6 +60,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// shared -> global TMA bulk store, tracked by the issuing thread's bulk group
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -2048,6 +2055,11 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const bool mine = valid && (lane >> 4) == h;
+            if constexpr (LEAN) {
+              // the previous half's bulk store has read the staging rows
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+            }
             if (mine) {
               float* row = stage + (lane & 15) * D;
               if (ablate_bits(L) & 4u) {
@@ -2065,6 +2077,17 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
                   return j;
                 });
               }
+            }
+            if constexpr (LEAN) {
+              // one TMA bulk store per half-warp block (16-B aligned: A % 4
+              // == 0 and halves start at multiples of 16 rows)
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              const unsigned hmask = (vmask >> (16 * h)) & 0xffffu;
+              const int r0 = __shfl_sync(0xffffffffu, myrow, 16 * h);
+              if (lane == 0 && hmask != 0u)
+                bulk_s2g(cta_out + static_cast<int64_t>(r0) * D, stage, static_cast<uint32_t>(__popc(hmask) * D * 4));
+              continue;
             }
             __syncwarp();
             const unsigned hm = (vmask >> (16 * h)) & 0xffffu;
@@ -2087,12 +2110,24 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
             __syncwarp();
           }
         }
+        if constexpr (LEAN) {
+          if (lane == 0) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+          __syncwarp();
+        }
         goto obs_done;
       }
     }
     for (int base = 0; base < A; base += tpe) {
       const int a = base + lt;
       const bool valid = live && a < A;
+      if constexpr (LEAN) {
+        // the previous pass's bulk store has read the staging rows
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      }
       if (valid) {
         float* row = stage + lane * D;
         const int cl = cell_lists ? s.cellof[a] : 0;
@@ -2151,6 +2186,19 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
           write_row<CONT, 0>(s, p, sc.step_count, a, row, [&](int n) { return n < a ? n : n + 1; });
         }
       }
+      if constexpr (LEAN) {
+        // One TMA bulk store per warp: its valid rows are one block, 16-B
+        // aligned in both spaces (A % 4 == 0 and warps start at multiples of
+        // 32 rows, so blocks start and end on 4-row boundaries: 16 * D
+        // bytes). Each lane's staged row is fenced into the async proxy
+        // before the store reads it.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (lane == 0 && vm != 0u)
+          bulk_s2g(cta_out + static_cast<int64_t>(a) * D, stage, static_cast<uint32_t>(__popc(vm) * D * 4));
+        continue;
+      }
       __syncwarp();
       // Rows of this warp in CTA-row space (row = le * A + a); when the valid
       // lanes form a prefix (always, except masked reinit of packed envs) the
@@ -2172,6 +2220,15 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
       } else if (valid) {
         float* dst = cta_out + static_cast<int64_t>(myrow) * D;
         for (int f = 0; f < D; ++f) st_rows(dst + f, stage[lane * D + f]);
+      }
+      __syncwarp();
+    }
+    if constexpr (LEAN) {
+      // the warp's bulk stores have landed (and their smem is free) before the
+      // CTA publishes the env (PDL flags) or exits
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       __syncwarp();
     }
