@@ -2369,6 +2369,9 @@ obs_done:
 // Same arithmetic as the main kernel (sample_tag_row, move_regs, d2_of, the
 // write_obs_row formulas, the fused reset), so results are bit-identical.
 constexpr int kSmallThreads = 64;
+// floats per warp of the SMALL kernel's staging: the warp's rows plus up to 3
+// floats of alignment shift, rounded to 16 B
+__host__ __device__ constexpr int small_stage_floats(int warp_floats) { return (warp_floats + 3 + 3) / 4 * 4; }
 
 template <bool CONT>
 __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevConfig p, const TagDevArrays g,
@@ -2380,7 +2383,12 @@ __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevCo
   const int lane = threadIdx.x & 31;
   const int A = p.A;
   const int epw = 32 / A;  // envs per warp
-  float* stage = small_stage + (threadIdx.x >> 5) * (epw * A * p.D);
+  // Per-warp staging block, shifted by the block's float offset from a 16-B
+  // boundary of the obs array so that staging and destination share their
+  // alignment (the copy-out is a TMA bulk store between scalar head/tail).
+  const int64_t wrow0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31)) >> 5) * epw * A;
+  const int mis = static_cast<int>((wrow0 * p.D) & 3);
+  float* stage = small_stage + (threadIdx.x >> 5) * small_stage_floats(epw * A * p.D) + mis;
   auto st_sm = [](float* q, float v) { *q = v; };
   const int le = lane / A, la = lane - le * A;
   const int64_t wg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -2556,6 +2564,9 @@ __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevCo
       sn = sin_ref(dir);
       cs = cos_ref(dir);
     }
+    // the previous step's bulk store has read the staging rows
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
     float* out = stage + lane * p.D;  // this warp's staging rows: row == lane
     const float iw = p.inv_world;
     const int vis = A - 1;
@@ -2615,25 +2626,23 @@ __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevCo
         }
       }
     }
-    // the warp's rows are one contiguous block of the obs array: coalesced
-    // streaming stores (16-byte where aligned)
+    // the warp's rows are one contiguous block of the obs array: a scalar
+    // head up to the first 16-B boundary, one TMA bulk store of the aligned
+    // body (staging and destination share their alignment), a scalar tail
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     {
       const int nrows = __popc(__ballot_sync(0xffffffffu, valid));
       const int nf = nrows * p.D;
       const int64_t f0 = (wg * epw * A) * static_cast<int64_t>(p.D);
       float* dst = g.obs + f0;
-      const int align = static_cast<int>((4 - (f0 & 3)) & 3);  // floats until dst is 16-B aligned
+      const int align = (4 - mis) & 3;  // floats until dst (and stage) are 16-B aligned
       const int head = align < nf ? align : nf;
+      const int body = ((nf - head) >> 2) << 2;
       if (lane < head) st_rows(dst + lane, stage[lane]);
-      const int nv = (nf - head) >> 2;
-      const float* sv = stage + head;
-      float4* dv = reinterpret_cast<float4*>(dst + head);
-      for (int v = lane; v < nv; v += 32)
-        st_rows(dv + v, make_float4(sv[4 * v], sv[4 * v + 1], sv[4 * v + 2], sv[4 * v + 3]));
-      for (int f = head + 4 * nv + lane; f < nf; f += 32) st_rows(dst + f, stage[f]);
+      if (lane == 0 && body > 0) bulk_s2g(dst + head, stage + head, static_cast<uint32_t>(body * 4));
+      for (int f = head + body + lane; f < nf; f += 32) st_rows(dst + f, stage[f]);
     }
-    __syncwarp();
   }
   if (valid) {
     g.loc_x[ia] = x;
@@ -2645,6 +2654,7 @@ __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevCo
     g.active[ia] = act ? 1 : 0;
   }
   if (nonfinite && L.error) atomicOr(L.error, kErrNonFinite);
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // smem stays valid until read
 }
 
 // ---- standalone sampler: sample_actions (sampler.cpp:5-40) ----------------
@@ -2878,7 +2888,7 @@ cudaError_t launch_small(const TagDevConfig& p, const TagDevArrays& g, const Tag
   const int64_t wpb = kSmallThreads / 32;
   const unsigned blocks = static_cast<unsigned>((warps + wpb - 1) / wpb);
   auto kern = tag_small_kernel<CONT>;
-  const size_t smem = static_cast<size_t>(wpb) * epw * p.A * p.D * sizeof(float);
+  const size_t smem = static_cast<size_t>(wpb) * small_stage_floats(static_cast<int>(epw * p.A * p.D)) * sizeof(float);
   if (smem > 48 * 1024) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (err != cudaSuccess) return err;
