@@ -464,7 +464,9 @@ __device__ int cell_knn(const EnvSmem& s, const TagDevConfig& p, int c, uint16_t
 // lowest-index tagger of each cell comes from an atomicMin while counting,
 // the per-cell K-NN lists insert (d2, index) keys, and find_tagger's cell scan
 // takes the minimum index. Thread t owns agents 4t..4t+3 (A % 4 == 0).
-constexpr int kCellQCount = 64;  // scratch int slot: build_cell_lists_keys' queue length
+// scratch int slot of build_cell_lists_keys' queue length: past the tracker's
+// per-warp double slots (kSlotT / kSlotR for up to 32 warps: ints 32..159)
+constexpr int kCellQCount = 160;
 
 __device__ void build_grid_lattice(const EnvSmem& s, const TagDevConfig& p, int* scratch, bool mark_active) {
   const int nthr = blockDim.x, tid = threadIdx.x;
