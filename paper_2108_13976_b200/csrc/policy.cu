@@ -284,12 +284,51 @@ static_assert(bf_image_bytes(16) % 16 == 0 && bf_image_bytes(32) % 16 == 0 && bf
               "image size");
 constexpr int kBfTmemCols = 64;  // D1, D2 and the head all live in columns [0, 64)
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // sample_from_logits (sampler.hpp:18-30) on V register logits.
+// The decision is first taken on f32 estimates (ex2.approx, MUFU) with a
+// rigorous margin. Each estimate of exp(dd), dd = z - zmax <= 0, carries a
+// relative error below |dd| 1.8e-7 (three f32 roundings of dd log2 e) plus
+// 2^-22 (ex2.approx), i.e. an absolute error below 3.1e-7 since
+// |dd| exp(dd) <= 1/e and total >= 1; with the f32 sums and the rounding of
+// u, target and every cumulative sum stay within 4e-6 x total of their f64
+// values. When no cumulative sum lies within 1e-5 x total of the target the
+// f64 path (the reference arithmetic) picks the same action; it runs only
+// for the rare rows that close.
 template <int V>
 __device__ __forceinline__ int sample_row_regs(const double* z, double u) {
   double zmax = z[0];
 #pragma unroll
   for (int i = 1; i < V; ++i) zmax = zmax < z[i] ? z[i] : zmax;
+  {
+    float evf[V], totf = 0.0f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float dd = static_cast<float>(z[i] - zmax);
+      evf[i] = dd == 0.0f ? 1.0f : ex2_approx(dd * 1.4426950408889634f);
+      totf += evf[i];
+    }
+    const float tgt = static_cast<float>(u) * totf;
+    const float margin = 1e-5f * totf;
+    float cum = 0.0f;
+    int pick = V - 1;
+    bool found = false, close = false;
+#pragma unroll
+    for (int i = 0; i + 1 < V; ++i) {
+      cum += evf[i];
+      close |= fabsf(tgt - cum) <= margin;
+      if (!found && tgt < cum) {
+        pick = i;
+        found = true;
+      }
+    }
+    if (!close) return pick;
+  }
   double ev[V], total = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
