@@ -1131,6 +1131,39 @@ __device__ __forceinline__ void load_row5(const double* __restrict__ z, int64_t 
   }
 }
 
+// The sampling decision on f32 estimates (ex2.approx) with a rigorous margin
+// (the bound is derived at policy.cu's sample_row_regs: estimates within
+// 4e-6 x total of the f64 target and cumulative sums); returns false when a
+// cumulative sum lies within 1e-5 x total of the target, and the caller then
+// runs the reference f64 arithmetic. Rows of equal logits need no exp.
+template <int V>
+__device__ __forceinline__ bool sample_fast(const double* z, double zmax, double u, int32_t& pick) {
+  float evf[V], totf = 0.0f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const float dd = static_cast<float>(z[i] - zmax);
+    float e = 1.0f;
+    if (dd != 0.0f) asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(dd * 1.4426950408889634f));
+    evf[i] = e;
+    totf += e;
+  }
+  const float tgt = static_cast<float>(u) * totf;
+  const float margin = 1e-5f * totf;
+  float cum = 0.0f;
+  bool found = false, close = false;
+  pick = V - 1;
+#pragma unroll
+  for (int i = 0; i + 1 < V; ++i) {
+    cum += evf[i];
+    close |= fabsf(tgt - cum) <= margin;
+    if (!found && tgt < cum) {
+      pick = i;
+      found = true;
+    }
+  }
+  return !close;
+}
+
 // sample_from_logits (sampler.hpp:18-30) on a register row of 5.
 __device__ __forceinline__ int32_t sample5(const double* z, double u, bool& nonfinite) {
   double zmax = z[0];
@@ -1138,6 +1171,10 @@ __device__ __forceinline__ int32_t sample5(const double* z, double u, bool& nonf
   for (int i = 0; i < 5; ++i) {
     nonfinite |= !isfinite(z[i]);
     zmax = zmax < z[i] ? z[i] : zmax;
+  }
+  {
+    int32_t fast;
+    if (sample_fast<5>(z, zmax, u, fast)) return fast;
   }
   double ev[5];
   double total = 0.0;
@@ -1184,6 +1221,10 @@ __device__ __forceinline__ int32_t sample_tag_row(const double* __restrict__ log
       nonfinite |= !isfinite(z[i]);
       zmax = zmax < z[i] ? z[i] : zmax;
     }
+    {
+      int32_t fast;
+      if (sample_fast<V>(z, zmax, u, fast)) return fast;
+    }
     double ev[V];
     double total = 0.0;
 #pragma unroll
@@ -1220,6 +1261,10 @@ __device__ __forceinline__ int32_t sample_regs(const double* z, double u, bool& 
     for (int i = 0; i < V; ++i) {
       nonfinite |= !isfinite(z[i]);
       zmax = zmax < z[i] ? z[i] : zmax;
+    }
+    {
+      int32_t fast;
+      if (sample_fast<V>(z, zmax, u, fast)) return fast;
     }
     double ev[V];
     double total = 0.0;
