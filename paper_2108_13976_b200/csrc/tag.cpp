@@ -53,6 +53,7 @@ constexpr TuningKey kTuningKeys[] = {
     {"l2_prefetch", "WDG_L2_PREFETCH"},           // env stride of an L2 prefetch of later inputs
     {"pdl_mode", "WDG_PDL"},                      // launch overlap, TagPlan::pdl_mode values
     {"multistep", "WDG_MULTISTEP"},               // 0: no multi-step residency in run()
+    {"cont_keys", "WDG_CONT_KEYS"},               // continuous K=5: 1 keyed ring search, 0 exact only
 };
 constexpr int kNumTuning = static_cast<int>(sizeof(kTuningKeys) / sizeof(kTuningKeys[0]));
 int64_t* tuning_table() {
@@ -285,6 +286,9 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     p.gc = std::max(1, std::min(static_cast<int>(std::floor(std::sqrt(static_cast<double>(A) / div))), 128));
     p.cell_inv = static_cast<float>(static_cast<double>(p.gc) / cfg.world_length);
     p.cell_size = cfg.world_length / p.gc;
+    // keyed ring search (LEAN, 2000 envs, us/step exact / keyed): A = 300
+    // 146.5 / 156.6, 500 200.1 / 191.2, 1000 332.8 / 314.4
+    p.cont_keys = tuning("cont_keys", A >= 500 ? 1 : 0) != 0 ? 1 : 0;
   } else {
     p.gc = static_cast<int32_t>(std::min<int64_t>(cfg.grid_size, std::min(sq, 128)));
     if (lattice_fits) p.gc = static_cast<int32_t>(g);

@@ -791,6 +791,80 @@ __device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<M
   }
 }
 
+// Continuous ring search with 32-bit keys: the same rings, bounds and cell
+// pruning as knn_rings, but a candidate is (truncated d2 bits << b | index,
+// b = index bits): one unsigned compare admits it, and an admitted key enters
+// a branchless min/max chain of K + 1 keys instead of the (d2, index) shift
+// network. The kept order is the exact (d2, index) order of the first K
+// whenever the K + 1 kept keys have strictly increasing truncated d2
+// (truncation is monotone: every other candidate, visited or not, then has a
+// strictly larger truncated and so exact d2; the ring bound and the pruning
+// use an upper bound of the K-th d2). Otherwise (an exact tie or a relative
+// gap below 2^-(23-b)) it returns false and the caller runs the exact search.
+template <int MAXK, bool EXACT>
+__device__ __forceinline__ bool knn_rings_keys(const EnvSmem& s, const TagDevConfig& p, int a,
+                                               TopK<MAXK, EXACT>& top) {
+  constexpr int KK = MAXK + 1;
+  const int b = 32 - __clz(max(p.A - 1, 1));
+  const int S = b - 1;  // (31 - S) d2 bits + b index bits = 32
+  uint32_t l[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) l[t] = 0xffffffffu;
+  const float sx = s.x[a], sy = s.y[a];
+  const int gc = p.gc;
+  const int cx = cell_coord<true>(sx, p), cy = cell_coord<true>(sy, p);
+  const int maxr = max(max(cx, gc - 1 - cx), max(cy, gc - 1 - cy));
+  const double cs = p.cell_size;
+  const double edge_in = fmax(0.0, fmin(fmin(static_cast<double>(sx) - cx * cs, (cx + 1) * cs - sx),
+                                        fmin(static_cast<double>(sy) - cy * cs, (cy + 1) * cs - sy)) -
+                                       1e-3 * cs);
+  for (int r = 0; r <= maxr; ++r) {
+    const float wd_up = __uint_as_float(min(((l[MAXK - 1] >> b) + 1u) << S, 0x7f800000u));
+    if (r > 0 && l[MAXK - 1] != 0xffffffffu) {
+      const double lb = fmax(0.0, (r - 1) - 1e-3) * cs + edge_in;
+      if (wd_up < static_cast<float>(lb * lb * (1.0 - 1e-5))) break;
+    }
+    const int y0 = cy - r, y1 = cy + r, x0 = cx - r, x1 = cx + r;
+    for (int gy = max(y0, 0); gy <= min(y1, gc - 1); ++gy) {
+      const bool edge = (gy == y0 || gy == y1);
+      const int step = edge ? 1 : max(x1 - x0, 1);
+      for (int gx = x0; gx <= x1; gx += step) {
+        if (gx < 0 || gx >= gc) continue;
+        if (r > 1 && l[MAXK - 1] != 0xffffffffu) {
+          const double lo_x = (gx - 1e-3) * cs, hi_x = (gx + 1 + 1e-3) * cs;
+          const double lo_y = (gy - 1e-3) * cs, hi_y = (gy + 1 + 1e-3) * cs;
+          const double dx = fmax(0.0, fmax(lo_x - sx, sx - hi_x));
+          const double dy = fmax(0.0, fmax(lo_y - sy, sy - hi_y));
+          if (static_cast<float>((dx * dx + dy * dy) * (1.0 - 1e-5)) > wd_up) continue;
+        }
+        const int c = gy * gc + gx;
+        const int e = s.cstart[c + 1];
+        for (int t = s.cstart[c]; t < e; ++t) {
+          const int j = s.items[t];
+          const uint32_t d2b = __float_as_uint(d2_of(sx, sy, s.x[j], s.y[j]));
+          uint32_t key = ((d2b >> S) << b) | static_cast<uint32_t>(j);
+          if (j == a || key >= l[KK - 1]) continue;
+#pragma unroll
+          for (int q = 0; q < KK; ++q) {
+            const uint32_t lo = min(l[q], key);
+            key = max(l[q], key);
+            l[q] = lo;
+          }
+        }
+      }
+    }
+  }
+  bool strict = true;
+#pragma unroll
+  for (int q = 0; q + 1 < KK; ++q)
+    strict &= l[q + 1] == 0xffffffffu || (l[q] >> b) < (l[q + 1] >> b);
+  if (!strict) return false;
+  const uint32_t low = (1u << b) - 1u;
+#pragma unroll
+  for (int t = 0; t < MAXK; ++t) top.i[t] = static_cast<int>(l[t] & low);
+  return true;
+}
+
 // Discrete lattice search: shells of equal integer d2 in increasing order.
 // Candidates need no coordinate reads (d2 is the shell's). Falls back to the
 // ring search if the precomputed disk is exhausted (very sparse envs).
@@ -904,6 +978,9 @@ __device__ __forceinline__ void knn_agent(const EnvSmem& s, const TagDevConfig& 
   if (!CONT && lattice_ok) {
     knn_lattice<MAXK, EXACT>(s, p, a, top);
     return;
+  }
+  if constexpr (CONT && EXACT) {
+    if (p.cont_keys && knn_rings_keys<MAXK, EXACT>(s, p, a, top)) return;
   }
   knn_rings<CONT, MAXK, EXACT>(s, p, a, top, integral);
 }

@@ -102,6 +102,9 @@ struct TagDevConfig {
   // 65535 agents, or more than 227 KB of shared memory per env) run on the
   // global-memory TagReference kernels (twin_kernels.cu) instead.
   int32_t fallback = 0;
+  // continuous K = 5 ring search on 32-bit (truncated d2, index) keys, exact
+  // search only where the kept keys tie (knn_rings_keys)
+  int32_t cont_keys = 0;
 };
 
 // Per-launch arguments.

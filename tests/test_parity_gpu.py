@@ -716,3 +716,41 @@ def test_fused_sampler_near_boundary_rows_bit_exact(cont):
     assert d is None, f"first divergence {d}"
     drv.check()
     ws.close()
+
+
+@pytest.mark.parametrize("keys", [0, 1])
+@pytest.mark.parametrize("ties", [False, True])
+@pytest.mark.parametrize("kw,envs", [
+    (dict(num_taggers=2, num_runners=10, world_length=8.0, seed=4), 20),
+    (dict(num_taggers=60, num_runners=240, world_length=12.0, tag_radius=0.6, seed=5), 3),
+    (dict(num_taggers=120, num_runners=480, world_length=20.0, tag_radius=0.5, seed=7), 2),
+])
+def test_continuous_keyed_ring_search_bit_exact(kw, envs, ties, keys):
+    """Continuous partial K-NN with the keyed ring search forced on or off
+    (tuning key cont_keys; the plan enables it from 500 agents): fused steps
+    bit-exact vs the oracle. ties=True pushes integral positions first, so
+    equal d2 abound and the keyed search must hand those agents to the exact
+    one (neighbor_grid.hpp:62-111 order: (d2, index))."""
+    dc, oc = cfg_pair(variant=O.CONTINUOUS, obs_mode=O.PARTIAL, k_nearest=5, episode_length=30, **kw)
+    W.set_tuning("cont_keys", keys)
+    try:
+        ws = W.Workspace(dc, envs)
+        o = O.OracleWorld(oc, envs)
+        if ties:
+            for n in ("loc_x", "loc_y"):
+                v = np.floor(o.pull(n))
+                o.push(n, v)
+                ws.store.push(n, v)
+        A = dc.num_agents()
+        lg = np.random.default_rng(11).normal(0, 1.5, (envs, A, 2, 3))
+        drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, oc.seed)
+        drv.set_logits(to_dev(lg), lg.size)
+        for t in range(12):
+            drv.step()
+            o.rollout(t, 1, oc.seed, lg)
+            d = O.first_divergence({n: ws.store.pull(n) for n in o.layout}, o.snapshot())
+            assert d is None, f"step {t}: first divergence {d}"
+        drv.check()
+        ws.close()
+    finally:
+        W.set_tuning("cont_keys", -1)
