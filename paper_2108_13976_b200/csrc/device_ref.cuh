@@ -93,6 +93,38 @@ __device__ __forceinline__ float sincosf_ref(float y, bool want_cos) {
 }
 __device__ __forceinline__ float sin_ref(float v) { return sincosf_ref(v, false); }
 __device__ __forceinline__ float cos_ref(float v) { return sincosf_ref(v, true); }
+// sin_ref and cos_ref of one value with one range reduction: the same steps
+// as the two calls (the quadrant's table and sign serve both; one of the two
+// takes the cos polynomial, the other the signed sin polynomial).
+__device__ __forceinline__ void sincos_ref(float y, float& sn, float& cs) {
+  const uint32_t top = (__float_as_uint(y) >> 20) & 0x7ffu;
+  const double x = static_cast<double>(y);
+  if (top <= 0x3f3u) {  // |y| < pi/4
+    if (top <= 0x397u) {
+      sn = y;
+      cs = 1.0f;
+      return;
+    }
+    const double x2 = __dmul_rn(x, x);
+    sn = __double2float_rn(sinf_poly(x, x2, c_sincos[0]));
+    cs = __double2float_rn(cosf_poly(x2, c_sincos[0]));
+    return;
+  }
+  if (top > 0x42eu) {  // |y| >= 120: outside the replica (not reachable from the env)
+    sn = __double2float_rn(sin(x));
+    cs = __double2float_rn(cos(x));
+    return;
+  }
+  const int n = (__double2int_rz(__dmul_rn(x, c_sincos[0].hpi_inv)) + 0x800000) >> 24;
+  const double r = __fma_rn(-static_cast<double>(n), c_sincos[0].hpi, x);
+  const SinCosTab& p = c_sincos[(n & 2) ? 1 : 0];
+  const double x2 = __dmul_rn(r, r);
+  const double sign = ((n + 1) & 2) ? -1.0 : 1.0;  // sign[n & 3] = {1, -1, -1, 1}
+  const float cp = __double2float_rn(cosf_poly(x2, p));
+  const float sp = __double2float_rn(sinf_poly(__dmul_rn(r, sign), x2, p));
+  sn = (n & 1) ? cp : sp;
+  cs = (n & 1) ? sp : cp;
+}
 
 }  // namespace
 }  // namespace wdg

@@ -1393,8 +1393,10 @@ __device__ __forceinline__ void move_regs(const TagDevConfig& p, int a, int act0
     if (act0 == 2) sp = __fadd_rn(sp, p.accel_delta);
     const float ms = a < p.T ? p.max_speed_tagger : p.max_speed_runner;
     sp = min_ref(max_ref(sp, 0.0f), ms);
-    x = min_ref(max_ref(__fadd_rn(x, __fmul_rn(sp, cos_ref(dir))), 0.0f), p.world_hi);
-    y = min_ref(max_ref(__fadd_rn(y, __fmul_rn(sp, sin_ref(dir))), 0.0f), p.world_hi);
+    float sn, cs;
+    sincos_ref(dir, sn, cs);
+    x = min_ref(max_ref(__fadd_rn(x, __fmul_rn(sp, cs)), 0.0f), p.world_hi);
+    y = min_ref(max_ref(__fadd_rn(y, __fmul_rn(sp, sn)), 0.0f), p.world_hi);
   }
 }
 
@@ -2011,8 +2013,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
     if (single && !reset_now) {
       if (CONT) {
         for (int a = lt; a < A; a += tpe) {
-          s.sn[a] = sin_ref(s.dir[a]);
-          s.cs[a] = cos_ref(s.dir[a]);
+          sincos_ref(s.dir[a], s.sn[a], s.cs[a]);
         }
       }
       if (PARTIAL && !CONT && GRID && p.lattice && all_integral) {
@@ -2119,8 +2120,7 @@ __global__ void __launch_bounds__(kMaxThreadsPerCta, env_min_blocks(CONT, MAXK))
   const bool early_inputs = single && mode != kModeReinit && !place;
   if (CONT && live && !early_inputs) {
     for (int a = lt; a < A; a += tpe) {
-      s.sn[a] = sin_ref(s.dir[a]);
-      s.cs[a] = cos_ref(s.dir[a]);
+      sincos_ref(s.dir[a], s.sn[a], s.cs[a]);
     }
   }
   // single-env CTA: `place` is CTA-uniform here (every thread has le == 0)
@@ -2712,8 +2712,7 @@ __global__ void __launch_bounds__(kSmallThreads) tag_small_kernel(const TagDevCo
     // (post-reset) state: every other agent in ascending order
     float sn = 0.f, cs = 0.f;
     if (CONT) {
-      sn = sin_ref(dir);
-      cs = cos_ref(dir);
+      sincos_ref(dir, sn, cs);
     }
     // the previous step's bulk store has read the staging rows
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
