@@ -286,9 +286,11 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     p.gc = std::max(1, std::min(static_cast<int>(std::floor(std::sqrt(static_cast<double>(A) / div))), 128));
     p.cell_inv = static_cast<float>(static_cast<double>(p.gc) / cfg.world_length);
     p.cell_size = cfg.world_length / p.gc;
-    // keyed ring search (LEAN, 2000 envs, us/step exact / keyed): A = 300
-    // 146.5 / 156.6, 500 200.1 / 191.2, 1000 332.8 / 314.4
-    p.cont_keys = tuning("cont_keys", A >= 500 ? 1 : 0) != 0 ? 1 : 0;
+    // keyed ring search (LEAN, 2000 envs, us/step exact / keyed,
+    // tools/keys_scan.py): A = 300 133.7 / 137.3, 400 155.1 / 158.0, 450
+    // 202.3 / 198.2, 500 181.7 / 172.9, 700 236.3 / 223.6, 1000 305.0 / 292.4
+    // — it wins on the CTAs wider than 128 threads (A > 400, rule below)
+    p.cont_keys = tuning("cont_keys", A > 400 ? 1 : 0) != 0 ? 1 : 0;
   } else {
     p.gc = static_cast<int32_t>(std::min<int64_t>(cfg.grid_size, std::min(sq, 128)));
     if (lattice_fits) p.gc = static_cast<int32_t>(g);

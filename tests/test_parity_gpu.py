@@ -727,7 +727,7 @@ def test_fused_sampler_near_boundary_rows_bit_exact(cont):
 ])
 def test_continuous_keyed_ring_search_bit_exact(kw, envs, ties, keys):
     """Continuous partial K-NN with the keyed ring search forced on or off
-    (tuning key cont_keys; the plan enables it from 500 agents): fused steps
+    (tuning key cont_keys; the plan enables it above 400 agents): fused steps
     bit-exact vs the oracle. ties=True pushes integral positions first, so
     equal d2 abound and the keyed search must hand those agents to the exact
     one (neighbor_grid.hpp:62-111 order: (d2, index))."""
