@@ -134,7 +134,7 @@ namespace {
 constexpr int kNumSMs = 148;
 constexpr int kBruteMaxAgents = 64;    // brute-force K-NN/resolve up to this (full obs)
 constexpr int kBruteMaxPartialDisc = 192;  // ... partial obs, discrete without lattice cells
-constexpr int kBruteMaxPartialCont = 200;  // ... partial obs, continuous
+constexpr int kBruteMaxPartialCont = 176;  // ... partial obs, continuous
 constexpr int kMaxSmem = 227 * 1024;
 
 int32_t round_up(int64_t v, int64_t m) { return static_cast<int32_t>((v + m - 1) / m * m); }
@@ -232,6 +232,9 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   // 256 178 vs 146 -> brute up to 200):
   // discrete A = 100 41 vs 76, 160 63 vs 140 (ring), 256 121 vs 99 (lattice);
   // continuous A = 100 63 vs 103, 200 148 vs 192, 256 185 vs 196.
+  // Continuous after the flattened 3 x 3 block scan with paired key
+  // insertion (tools/tune_scan.py, brute vs grid): A = 100 55.7 vs 70.8,
+  // 150 85.6 vs 100.2, 170 99.9 vs 108.3, 200 138.8 vs 103.3 -> brute to 176.
   int brute_max = !p.partial ? kBruteMaxAgents
                   : p.continuous ? kBruteMaxPartialCont
                   : lattice_fits ? kBruteMaxAgents : kBruteMaxPartialDisc;
@@ -278,10 +281,13 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   // Bucket grid: ~1 agent per cell, lattice cells for discrete when possible.
   const int sq = std::max(1, static_cast<int>(std::floor(std::sqrt(static_cast<double>(A)))));
   if (p.continuous) {
-    // ~3 agents per cell: the K=5 nearest then mostly sit within ring 1
-    // (fewer cells per query). Measured at A = 100 / 1000: 1 agent per cell
-    // 128 / 537 us/step, 2: 107 / 467, 3: 101 / 446, 4: 101 / 451.
-    int div = 3;
+    // ~4 agents per cell: the K=5 nearest then mostly sit within the 3 x 3
+    // block (one flattened scan, knn_rings_keys). Measured with that scan
+    // (tools/tune_scan.py, us/step at div 2 / 3 / 4 / 5 / 6 / 8): A = 1000
+    // 285.2 / 264.2 / 250.7 / 251.9 / 265.9 / 280.4, 500 168.1 / 157.6 /
+    // 154.2 / 153.2 / 155.6, 700 - / 196.5 / 191.7 / 195.1, 300 (keyed)
+    // 141.3 / 130.1 / 122.2 / 121.3 / 121.2. (Round 1, per-cell rings: 3.)
+    int div = 4;
     div = static_cast<int>(std::max<int64_t>(1, tuning("cont_cell_div", div)));
     p.gc = std::max(1, std::min(static_cast<int>(std::floor(std::sqrt(static_cast<double>(A) / div))), 128));
     p.cell_inv = static_cast<float>(static_cast<double>(p.gc) / cfg.world_length);
@@ -289,8 +295,11 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     // keyed ring search (LEAN, 2000 envs, us/step exact / keyed,
     // tools/keys_scan.py): A = 300 133.7 / 137.3, 400 155.1 / 158.0, 450
     // 202.3 / 198.2, 500 181.7 / 172.9, 700 236.3 / 223.6, 1000 305.0 / 292.4
-    // — it wins on the CTAs wider than 128 threads (A > 400, rule below)
-    p.cont_keys = tuning("cont_keys", A > 400 ? 1 : 0) != 0 ? 1 : 0;
+    // — it won on the CTAs wider than 128 threads (A > 400). With the
+    // flattened 3 x 3 block and paired insertion it wins on every grid shape
+    // (exact / keyed at div 4: A = 200 106.5 / 103.3, 300 129.5 / 122.2,
+    // 400 151.1 / 141.6), so grid plans always take it.
+    p.cont_keys = tuning("cont_keys", 1) != 0 ? 1 : 0;
   } else {
     p.gc = static_cast<int32_t>(std::min<int64_t>(cfg.grid_size, std::min(sq, 128)));
     if (lattice_fits) p.gc = static_cast<int32_t>(g);

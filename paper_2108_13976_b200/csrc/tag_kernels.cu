@@ -734,6 +734,37 @@ __device__ __forceinline__ float d2_of(float ax, float ay, float bx, float by) {
   return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
 }
 
+// Rings 0 and 1 of a ring search together: the 3 x 3 block around cell
+// (cx, cy) is at most 3 row ranges (the CSR is row-major, so cells gx0..gx1
+// of a row are contiguous in items), walked as ONE flattened loop: lanes
+// diverge on the block's total count instead of on 9 per-cell counts.
+// Visiting ring 1 without the ring-1 bound test only adds candidates, so a
+// search that keeps the exact smallest (d2, index) entries is unchanged.
+// put2 takes candidates two at a time (independent loads and keys in flight
+// together); put takes the odd one out.
+template <typename F, typename F2>
+__device__ __forceinline__ void scan_block3(const EnvSmem& s, int gc, int cx, int cy, F&& put, F2&& put2) {
+  const int gx0 = max(cx - 1, 0), gx1 = min(cx + 1, gc - 1);
+  const int gy0 = max(cy - 1, 0), gy1 = min(cy + 1, gc - 1);
+  const int* rs = s.cstart + gy0 * gc;
+  const int b0 = rs[gx0], e0 = rs[gx1 + 1];
+  int b1 = 0, e1 = 0, b2 = 0, e2 = 0;
+  if (gy0 + 1 <= gy1) {
+    b1 = rs[gc + gx0];
+    e1 = rs[gc + gx1 + 1];
+  }
+  if (gy0 + 2 <= gy1) {
+    b2 = rs[2 * gc + gx0];
+    e2 = rs[2 * gc + gx1 + 1];
+  }
+  const int n0 = e0 - b0, n01 = n0 + (e1 - b1), n = n01 + (e2 - b2);
+  const int d1 = b1 - n0, d2 = b2 - n01;
+  auto at = [&](int t) { return s.items[t + (t < n0 ? b0 : (t < n01 ? d1 : d2))]; };
+  int t = 0;
+  for (; t + 1 < n; t += 2) put2(at(t), at(t + 1));
+  if (t < n) put(at(t));
+}
+
 // Generic ring search over the bucket grid (continuous / non-lattice).
 template <bool CONT, int MAXK, bool EXACT>
 __device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<MAXK, EXACT>& top,
@@ -752,7 +783,16 @@ __device__ void knn_rings(const EnvSmem& s, const TagDevConfig& p, int a, TopK<M
                                                fmin(static_cast<double>(sy) - cy * cs, (cy + 1) * cs - sy)) -
                                                   1e-3 * cs)
                               : 0.0;
-  for (int r = 0; r <= maxr; ++r) {
+  if (CONT) {
+    auto put = [&](int j) {
+      if (j != a) top.consider(d2_of(sx, sy, s.x[j], s.y[j]), j);
+    };
+    scan_block3(s, gc, cx, cy, put, [&](int j0, int j1) {
+      put(j0);
+      put(j1);
+    });
+  }
+  for (int r = CONT ? 2 : 0; r <= maxr; ++r) {
     if (r > 0 && top.full()) {
       // Every point in rings >= r is farther than this bound (SURVEY.md §8a
       // a6; cf. the reference's ring margin, neighbor_grid.hpp:90-96).
@@ -819,9 +859,35 @@ __device__ __forceinline__ bool knn_rings_keys(const EnvSmem& s, const TagDevCon
   const double edge_in = fmax(0.0, fmin(fmin(static_cast<double>(sx) - cx * cs, (cx + 1) * cs - sx),
                                         fmin(static_cast<double>(sy) - cy * cs, (cy + 1) * cs - sy)) -
                                        1e-3 * cs);
-  for (int r = 0; r <= maxr; ++r) {
+  auto key_of = [&](int j) {
+    const uint32_t d2b = __float_as_uint(d2_of(sx, sy, s.x[j], s.y[j]));
+    return j == a ? 0xffffffffu : (((d2b >> S) << b) | static_cast<uint32_t>(j));
+  };
+  // branchless: a key above every kept one passes the chain unchanged
+  auto insert = [&](uint32_t key) {
+#pragma unroll
+    for (int q = 0; q < KK; ++q) {
+      const uint32_t lo = min(l[q], key);
+      key = max(l[q], key);
+      l[q] = lo;
+    }
+  };
+  auto put = [&](int j) {
+    const uint32_t key = key_of(j);
+    if (key < l[KK - 1]) insert(key);
+  };
+  // two keys per admission test: the second chain trails the first by one
+  // stage instead of waiting for it
+  scan_block3(s, gc, cx, cy, put, [&](int j0, int j1) {
+    const uint32_t k0 = key_of(j0), k1 = key_of(j1);
+    if (min(k0, k1) < l[KK - 1]) {
+      insert(k0);
+      insert(k1);
+    }
+  });  // rings 0 and 1
+  for (int r = 2; r <= maxr; ++r) {
     const float wd_up = __uint_as_float(min(((l[MAXK - 1] >> b) + 1u) << S, 0x7f800000u));
-    if (r > 0 && l[MAXK - 1] != 0xffffffffu) {
+    if (l[MAXK - 1] != 0xffffffffu) {
       const double lb = fmax(0.0, (r - 1) - 1e-3) * cs + edge_in;
       if (wd_up < static_cast<float>(lb * lb * (1.0 - 1e-5))) break;
     }
@@ -831,7 +897,7 @@ __device__ __forceinline__ bool knn_rings_keys(const EnvSmem& s, const TagDevCon
       const int step = edge ? 1 : max(x1 - x0, 1);
       for (int gx = x0; gx <= x1; gx += step) {
         if (gx < 0 || gx >= gc) continue;
-        if (r > 1 && l[MAXK - 1] != 0xffffffffu) {
+        if (l[MAXK - 1] != 0xffffffffu) {
           const double lo_x = (gx - 1e-3) * cs, hi_x = (gx + 1 + 1e-3) * cs;
           const double lo_y = (gy - 1e-3) * cs, hi_y = (gy + 1 + 1e-3) * cs;
           const double dx = fmax(0.0, fmax(lo_x - sx, sx - hi_x));
@@ -840,18 +906,7 @@ __device__ __forceinline__ bool knn_rings_keys(const EnvSmem& s, const TagDevCon
         }
         const int c = gy * gc + gx;
         const int e = s.cstart[c + 1];
-        for (int t = s.cstart[c]; t < e; ++t) {
-          const int j = s.items[t];
-          const uint32_t d2b = __float_as_uint(d2_of(sx, sy, s.x[j], s.y[j]));
-          uint32_t key = ((d2b >> S) << b) | static_cast<uint32_t>(j);
-          if (j == a || key >= l[KK - 1]) continue;
-#pragma unroll
-          for (int q = 0; q < KK; ++q) {
-            const uint32_t lo = min(l[q], key);
-            key = max(l[q], key);
-            l[q] = lo;
-          }
-        }
+        for (int t = s.cstart[c]; t < e; ++t) put(s.items[t]);
       }
     }
   }

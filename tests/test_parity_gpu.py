@@ -720,19 +720,26 @@ def test_fused_sampler_near_boundary_rows_bit_exact(cont):
 
 @pytest.mark.parametrize("keys", [0, 1])
 @pytest.mark.parametrize("ties", [False, True])
-@pytest.mark.parametrize("kw,envs", [
-    (dict(num_taggers=2, num_runners=10, world_length=8.0, seed=4), 20),
-    (dict(num_taggers=60, num_runners=240, world_length=12.0, tag_radius=0.6, seed=5), 3),
-    (dict(num_taggers=120, num_runners=480, world_length=20.0, tag_radius=0.5, seed=7), 2),
+@pytest.mark.parametrize("kw,envs,grid", [
+    (dict(num_taggers=2, num_runners=10, world_length=8.0, seed=4), 20, False),
+    # bucket grid forced on small envs: 1 x 1 and 3 x 3 cells, so the 3 x 3
+    # block scan clamps at every border
+    (dict(num_taggers=2, num_runners=10, world_length=8.0, seed=4), 20, True),
+    (dict(num_taggers=8, num_runners=32, world_length=6.0, tag_radius=0.7, seed=8), 6, True),
+    (dict(num_taggers=60, num_runners=240, world_length=12.0, tag_radius=0.6, seed=5), 3, False),
+    (dict(num_taggers=120, num_runners=480, world_length=20.0, tag_radius=0.5, seed=7), 2, False),
 ])
-def test_continuous_keyed_ring_search_bit_exact(kw, envs, ties, keys):
+def test_continuous_keyed_ring_search_bit_exact(kw, envs, grid, ties, keys):
     """Continuous partial K-NN with the keyed ring search forced on or off
-    (tuning key cont_keys; the plan enables it above 400 agents): fused steps
-    bit-exact vs the oracle. ties=True pushes integral positions first, so
-    equal d2 abound and the keyed search must hand those agents to the exact
-    one (neighbor_grid.hpp:62-111 order: (d2, index))."""
+    (tuning key cont_keys; the plan enables it on every grid plan): fused
+    steps bit-exact vs the oracle. ties=True pushes integral positions first,
+    so equal d2 abound and the keyed search must hand those agents to the
+    exact one (neighbor_grid.hpp:62-111 order: (d2, index)). Both searches
+    start with the flattened 3 x 3 block scan (scan_block3)."""
     dc, oc = cfg_pair(variant=O.CONTINUOUS, obs_mode=O.PARTIAL, k_nearest=5, episode_length=30, **kw)
     W.set_tuning("cont_keys", keys)
+    if grid:
+        W.set_tuning("brute_max", 1)
     try:
         ws = W.Workspace(dc, envs)
         o = O.OracleWorld(oc, envs)
@@ -750,7 +757,10 @@ def test_continuous_keyed_ring_search_bit_exact(kw, envs, ties, keys):
             o.rollout(t, 1, oc.seed, lg)
             d = O.first_divergence({n: ws.store.pull(n) for n in o.layout}, o.snapshot())
             assert d is None, f"step {t}: first divergence {d}"
+        if grid:
+            assert ws.plan.geometry()["uses_grid"] == 1
         drv.check()
         ws.close()
     finally:
         W.set_tuning("cont_keys", -1)
+        W.set_tuning("brute_max", -1)

@@ -32,11 +32,20 @@ def time_shape(var, A, K, E, steps=100):
 
 
 SCANS = [
-    ("disc160", (W.DISCRETE, 160, 5, 2000), "combo", [None, {"brute_max": 256}]),
-    ("disc176", (W.DISCRETE, 176, 5, 2000), "combo", [None, {"brute_max": 256}]),
-    ("disc192", (W.DISCRETE, 192, 5, 2000), "combo", [None]),
-    ("cont200", (W.CONTINUOUS, 200, 5, 2000), "combo", [None]),
-    ("cont240", (W.CONTINUOUS, 240, 5, 2000), "combo", [None, {"brute_max": 256}]),
+    # round 2, after the flattened 3 x 3 block + paired key insertion
+    ("cont170", (W.CONTINUOUS, 170, 5, 2000), "combo", [None, {"brute_max": 100, "cont_cell_div": 4},
+                                                        {"brute_max": 100, "cont_cell_div": 5}]),
+    ("cont200", (W.CONTINUOUS, 200, 5, 2000), "combo", [{"brute_max": 100, "cont_cell_div": 4},
+                                                        {"brute_max": 100, "cont_cell_div": 5},
+                                                        {"brute_max": 100, "cont_cell_div": 4, "cont_keys": 1}]),
+    ("cont300", (W.CONTINUOUS, 300, 5, 2000), "combo", [{"cont_cell_div": 4}, {"cont_keys": 1, "cont_cell_div": 5},
+                                                        {"cont_keys": 1, "cont_cell_div": 6}]),
+    ("cont400", (W.CONTINUOUS, 400, 5, 2000), "combo", [None, {"cont_keys": 1, "cont_cell_div": 4},
+                                                        {"cont_keys": 1, "cont_cell_div": 5}]),
+    ("cont500", (W.CONTINUOUS, 500, 5, 2000), "combo", [{"cont_cell_div": 5}, {"cont_cell_div": 6}]),
+    ("cont700", (W.CONTINUOUS, 700, 5, 2000), "combo", [None, {"cont_cell_div": 4}, {"cont_cell_div": 5}]),
+    ("cont1000", (W.CONTINUOUS, 1000, 5, 2000), "combo", [{"cont_cell_div": 4}, {"cont_cell_div": 5},
+                                                          {"cont_cell_div": 6}, {"cont_cell_div": 8}]),
 ]
 for name, shape, key, vals in SCANS:
     for v in vals:
