@@ -565,7 +565,26 @@ __device__ __forceinline__ int cell_knn_keys(const EnvSmem& s, const TagDevConfi
         continue;
       const int c2 = gy * g + gx;
       const int e = s.cstart[c2 + 1];
-      for (int t = s.cstart[c2]; t < e; ++t) {
+      int t = s.cstart[c2];
+      found += e - t;
+      // two keys per pass: the second min/max chain trails the first by one
+      // stage instead of waiting for its end
+      for (; t + 1 < e; t += 2) {
+        uint32_t k0 = hi | s.items[t], k1 = hi | s.items[t + 1];
+#pragma unroll
+        for (int q = 0; q < KK; ++q) {
+          const uint32_t lo = min(l[q], k0);
+          k0 = max(l[q], k0);
+          l[q] = lo;
+        }
+#pragma unroll
+        for (int q = 0; q < KK; ++q) {
+          const uint32_t lo = min(l[q], k1);
+          k1 = max(l[q], k1);
+          l[q] = lo;
+        }
+      }
+      if (t < e) {
         uint32_t key = hi | s.items[t];
 #pragma unroll
         for (int q = 0; q < KK; ++q) {
@@ -573,7 +592,6 @@ __device__ __forceinline__ int cell_knn_keys(const EnvSmem& s, const TagDevConfi
           key = max(l[q], key);
           l[q] = lo;
         }
-        ++found;
       }
     }
   }
