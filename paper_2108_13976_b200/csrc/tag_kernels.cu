@@ -981,11 +981,14 @@ __device__ __forceinline__ void knn_brute_keys(const EnvSmem& s, const TagDevCon
 #pragma unroll
   for (int t = 0; t < MAXK; ++t) k[t] = 0xffffffffu;
   const float sx = s.x[a], sy = s.y[a];
-  auto put = [&](int j) {
+  auto key_of = [&](int j) {
     const float dx = __fsub_rn(s.x[j], sx), dy = __fsub_rn(s.y[j], sy);
     const float d2 = __fmaf_rn(dx, dx, __fmul_rn(dy, dy));  // exact: integers below 2^16
-    // 2^23 + d2 holds d2 in its low mantissa bits
-    uint32_t key = __byte_perm(static_cast<uint32_t>(j), __float_as_uint(__fadd_rn(d2, 8388608.0f)), 0x5410);
+    // 2^23 + d2 holds d2 in its low mantissa bits; self never enters
+    const uint32_t key = __byte_perm(static_cast<uint32_t>(j), __float_as_uint(__fadd_rn(d2, 8388608.0f)), 0x5410);
+    return j == a ? 0xffffffffu : key;
+  };
+  auto insert = [&](uint32_t key) {
 #pragma unroll
     for (int t = 0; t < MAXK; ++t) {
       const uint32_t lo = min(k[t], key);
@@ -993,8 +996,14 @@ __device__ __forceinline__ void knn_brute_keys(const EnvSmem& s, const TagDevCon
       k[t] = lo;
     }
   };
-  for (int j = 0; j < a; ++j) put(j);
-  for (int j = a + 1; j < p.A; ++j) put(j);
+  // two candidates per pass: the second chain trails the first by one stage
+  int j = 0;
+  for (; j + 1 < p.A; j += 2) {
+    const uint32_t k0 = key_of(j), k1 = key_of(j + 1);
+    insert(k0);
+    insert(k1);
+  }
+  if (j < p.A) insert(key_of(j));
 #pragma unroll
   for (int t = 0; t < MAXK; ++t) out[t] = static_cast<int>(k[t] & 0xffffu);
 }
