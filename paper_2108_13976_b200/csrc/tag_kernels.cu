@@ -1008,6 +1008,51 @@ __device__ __forceinline__ void knn_brute_keys(const EnvSmem& s, const TagDevCon
   for (int t = 0; t < MAXK; ++t) out[t] = static_cast<int>(k[t] & 0xffffu);
 }
 
+// Brute-force K-NN over continuous positions with 32-bit keys (truncated d2
+// bits << b | index, b = index bits), as knn_rings_keys: two candidates per
+// pass through a branchless min/max chain of K + 1 keys. Exact whenever the
+// K + 1 kept keys have strictly increasing truncated d2 (every other
+// candidate then has a strictly larger exact d2); otherwise it returns false
+// and the caller runs knn_brute_pairs.
+template <int MAXK>
+__device__ __forceinline__ bool knn_brute_cont_keys(const EnvSmem& s, const TagDevConfig& p, int a, int* out) {
+  constexpr int KK = MAXK + 1;
+  const int b = 32 - __clz(max(p.A - 1, 1));
+  const int S = b - 1;  // (31 - S) d2 bits + b index bits = 32
+  uint32_t l[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) l[t] = 0xffffffffu;
+  const float sx = s.x[a], sy = s.y[a];
+  auto key_of = [&](int j) {
+    const uint32_t d2b = __float_as_uint(d2_of(sx, sy, s.x[j], s.y[j]));
+    return j == a ? 0xffffffffu : (((d2b >> S) << b) | static_cast<uint32_t>(j));
+  };
+  auto insert = [&](uint32_t key) {
+#pragma unroll
+    for (int q = 0; q < KK; ++q) {
+      const uint32_t lo = min(l[q], key);
+      key = max(l[q], key);
+      l[q] = lo;
+    }
+  };
+  int j = 0;
+  for (; j + 1 < p.A; j += 2) {
+    const uint32_t k0 = key_of(j), k1 = key_of(j + 1);
+    insert(k0);
+    insert(k1);
+  }
+  if (j < p.A) insert(key_of(j));
+  bool strict = true;
+#pragma unroll
+  for (int q = 0; q + 1 < KK; ++q)
+    strict &= l[q + 1] == 0xffffffffu || (l[q] >> b) < (l[q + 1] >> b);
+  if (!strict) return false;
+  const uint32_t low = (1u << b) - 1u;
+#pragma unroll
+  for (int t = 0; t < MAXK; ++t) out[t] = static_cast<int>(l[t] & low);
+  return true;
+}
+
 // Brute-force K-NN, any positions: ascending candidates, so (d2, index)
 // order is a strict d2 compare (ties keep the earlier index). The insertion
 // is a branchless shift: slots from the candidate's rank down move by one.
@@ -1047,7 +1092,7 @@ __device__ __forceinline__ void knn_agent(const EnvSmem& s, const TagDevConfig& 
   if (!GRID && MAXK <= 8) {
     if (!CONT && keys_ok)
       knn_brute_keys<MAXK>(s, p, a, top.i);
-    else
+    else if (!CONT || !p.cont_keys || !knn_brute_cont_keys<MAXK>(s, p, a, top.i))
       knn_brute_pairs<MAXK>(s, p, a, top.i);
     return;
   }
