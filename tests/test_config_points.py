@@ -11,6 +11,8 @@ paths bench.py and the sweeps time:
   wide-row writer, 16 MB of obs per env-step), 2 envs, every step.
 - C4: 1+4 agents, full obs, E in {1, 10000}, every step, single-step launches
   and run() windows (multi-step residency).
+- The sweep's continuous partial points (A in {100, 200, 1000}, 2000 envs) on
+  the same protocol as C3.
 Discrete Tag: bit-exact on every array."""
 import numpy as np
 import pytest
@@ -64,6 +66,39 @@ def test_c3_partial_2000_envs_bench_path(A, episode):
     assert st[W.STAT_ENV_STEPS] == 30 * E
     if episode == 6:
         assert st[W.STAT_EPISODES] >= E  # every env finished an episode
+    for e, o in worlds.items():
+        assert ws.resets.episodes_started(e) == o.episodes(0)
+    ws.close()
+
+
+@pytest.mark.parametrize("episode", [500, 6])
+@pytest.mark.parametrize("A", [100, 200, 1000])
+def test_continuous_partial_2000_envs_bench_path(A, episode):
+    """The sweep's continuous partial points on their launch path: A = 100
+    (brute force, 32-bit keys), 200 and 1000 (bucket grid, flattened 3 x 3
+    block scan with paired keys; LEAN at 1000). Same protocol as the C3 test:
+    20 back-to-back steps, then 10 checked one by one, sampled global env ids
+    re-run by the oracle, bit-exact on every array."""
+    T = int(np.floor(A / 5 + 0.5))
+    dc, oc = cfg_pair(variant=O.CONTINUOUS, num_taggers=T, num_runners=A - T, obs_mode=O.PARTIAL,
+                      k_nearest=5, episode_length=episode, seed=0)
+    E = 2000
+    ws = W.Workspace(dc, E)
+    drv = W.RolloutDriver(ws.store, ws.plan, ws.resets, oc.seed)
+    picks = (0, 443, 444, 1337, 1999)  # wave borders of 148 x 3 CTAs included
+    worlds = {e: O.OracleWorld(oc, 1, env_offset=e) for e in picks}
+    for _ in range(20):
+        drv.step()
+    for e, o in worlds.items():
+        o.rollout(0, 20, oc.seed)
+        envs_equal(ws, o, e, 1, "after 20 back-to-back steps")
+    for t in range(20, 30):
+        drv.step()
+        for e, o in worlds.items():
+            o.rollout(t, 1, oc.seed)
+            envs_equal(ws, o, e, 1, f"step {t}")
+    drv.check()
+    assert drv.stats()[W.STAT_ENV_STEPS] == 30 * E
     for e, o in worlds.items():
         assert ws.resets.episodes_started(e) == o.episodes(0)
     ws.close()
