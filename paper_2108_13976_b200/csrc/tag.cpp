@@ -251,8 +251,12 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     // 224, 600 263 / 240 / 260, 700 - / 292 / 270, 800 - / 342 / 290,
     // 1000 477 / 393 / 360. Smaller envs keep more CTAs (envs) per SM
     // overlapping each other's barriers; larger ones gain from wider CTAs.
+    // Discrete re-measured after the paired key insertion of the per-cell
+    // lists (us/step at 128 / 160 / 256 threads): A = 500 59.2 / 60.2 / 68.2,
+    // 600 70.3 / 63.7 / 73.1, 700 81.6 / 78.6 / 75.8, 800 88.2 / 83.4 / 80.3.
     int cap = 256;
-    if (p.partial && (p.continuous ? A <= 400 : A <= 448)) cap = 128;
+    if (p.partial && (p.continuous ? A <= 400 : A <= 560)) cap = 128;
+    else if (p.partial && !p.continuous && A <= 660) cap = 160;
     else if (p.partial && p.continuous && A <= 650) cap = 192;
     if (const int64_t t = tuning("threads_per_env_max", 0)) cap = static_cast<int>(std::clamp<int64_t>(t, 32, 1024)) / 32 * 32;
     cap = std::min(cap, kMaxThreadsPerCta);

@@ -41,7 +41,7 @@ def envs_equal(ws, o, e0, n, where):
 
 
 @pytest.mark.parametrize("episode", [500, 6])
-@pytest.mark.parametrize("A", [10, 100, 500, 1000])
+@pytest.mark.parametrize("A", [10, 100, 500, 600, 1000])  # 600: the 160-thread lattice CTA
 def test_c3_partial_2000_envs_bench_path(A, episode):
     T = int(np.floor(A / 5 + 0.5))
     dc, oc = cfg_pair(num_taggers=T, num_runners=A - T, obs_mode=O.PARTIAL, k_nearest=5,

@@ -32,20 +32,15 @@ def time_shape(var, A, K, E, steps=100):
 
 
 SCANS = [
-    # round 2, after the flattened 3 x 3 block + paired key insertion
-    ("cont170", (W.CONTINUOUS, 170, 5, 2000), "combo", [None, {"brute_max": 100, "cont_cell_div": 4},
-                                                        {"brute_max": 100, "cont_cell_div": 5}]),
-    ("cont200", (W.CONTINUOUS, 200, 5, 2000), "combo", [{"brute_max": 100, "cont_cell_div": 4},
-                                                        {"brute_max": 100, "cont_cell_div": 5},
-                                                        {"brute_max": 100, "cont_cell_div": 4, "cont_keys": 1}]),
-    ("cont300", (W.CONTINUOUS, 300, 5, 2000), "combo", [{"cont_cell_div": 4}, {"cont_keys": 1, "cont_cell_div": 5},
-                                                        {"cont_keys": 1, "cont_cell_div": 6}]),
-    ("cont400", (W.CONTINUOUS, 400, 5, 2000), "combo", [None, {"cont_keys": 1, "cont_cell_div": 4},
-                                                        {"cont_keys": 1, "cont_cell_div": 5}]),
-    ("cont500", (W.CONTINUOUS, 500, 5, 2000), "combo", [{"cont_cell_div": 5}, {"cont_cell_div": 6}]),
-    ("cont700", (W.CONTINUOUS, 700, 5, 2000), "combo", [None, {"cont_cell_div": 4}, {"cont_cell_div": 5}]),
-    ("cont1000", (W.CONTINUOUS, 1000, 5, 2000), "combo", [{"cont_cell_div": 4}, {"cont_cell_div": 5},
-                                                          {"cont_cell_div": 6}, {"cont_cell_div": 8}]),
+    # discrete lattice shapes after the paired key insertion (thread cap per env)
+    ("disc500", (W.DISCRETE, 500, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
+    ("disc600", (W.DISCRETE, 600, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
+    ("disc700", (W.DISCRETE, 700, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
+    ("disc800", (W.DISCRETE, 800, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
+    ("disc900", (W.DISCRETE, 900, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
+    ("cont500", (W.CONTINUOUS, 500, 5, 2000), "combo", [None, {"threads_per_env_max": 128}]),
+    ("cont700", (W.CONTINUOUS, 700, 5, 2000), "combo", [None, {"threads_per_env_max": 128}, {"threads_per_env_max": 192}]),
+    ("cont1000", (W.CONTINUOUS, 1000, 5, 2000), "combo", [None, {"threads_per_env_max": 128}, {"threads_per_env_max": 192}]),
 ]
 for name, shape, key, vals in SCANS:
     for v in vals:
