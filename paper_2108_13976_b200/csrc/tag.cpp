@@ -54,6 +54,7 @@ constexpr TuningKey kTuningKeys[] = {
     {"pdl_mode", "WDG_PDL"},                      // launch overlap, TagPlan::pdl_mode values
     {"multistep", "WDG_MULTISTEP"},               // 0: no multi-step residency in run()
     {"cont_keys", "WDG_CONT_KEYS"},               // continuous K=5: 1 keyed ring search, 0 exact only
+    {"packed_warps_max", "WDG_PACKED_WARPS"},     // warp cap of the packed (brute-force) CTA
 };
 constexpr int kNumTuning = static_cast<int>(sizeof(kTuningKeys) / sizeof(kTuningKeys[0]));
 int64_t* tuning_table() {
@@ -134,7 +135,7 @@ namespace {
 constexpr int kNumSMs = 148;
 constexpr int kBruteMaxAgents = 64;    // brute-force K-NN/resolve up to this (full obs)
 constexpr int kBruteMaxPartialDisc = 192;  // ... partial obs, discrete without lattice cells
-constexpr int kBruteMaxPartialCont = 176;  // ... partial obs, continuous
+constexpr int kBruteMaxPartialCont = 160;  // ... partial obs, continuous
 constexpr int kMaxSmem = 227 * 1024;
 
 int32_t round_up(int64_t v, int64_t m) { return static_cast<int32_t>((v + m - 1) / m * m); }
@@ -234,7 +235,9 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
   // continuous A = 100 63 vs 103, 200 148 vs 192, 256 185 vs 196.
   // Continuous after the flattened 3 x 3 block scan with paired key
   // insertion (tools/tune_scan.py, brute vs grid): A = 100 55.7 vs 70.8,
-  // 150 85.6 vs 100.2, 170 99.9 vs 108.3, 200 138.8 vs 103.3 -> brute to 176.
+  // 150 85.6 vs 100.2, 170 99.9 vs 108.3, 200 138.8 vs 103.3; after the
+  // continuous brute-force keys: 160 83.1 vs 89.7, 176 99.4 vs 96.0, 192
+  // 106.3 vs 97.2 -> brute to 160.
   int brute_max = !p.partial ? kBruteMaxAgents
                   : p.continuous ? kBruteMaxPartialCont
                   : lattice_fits ? kBruteMaxAgents : kBruteMaxPartialDisc;
@@ -267,7 +270,14 @@ TagDevConfig make_dev_config_rows(const DataStore& store, const wdg_tag_config& 
     // Smallest CTA (in warps) that holds >= 1 env, grown while the grid keeps
     // >= 2 CTAs per SM so small-A sweeps spread over all 148 SMs.
     int w = static_cast<int>((A + 31) / 32);
-    for (int cand = w; cand <= std::min(8, kMaxThreadsPerCta / 32); cand *= 2) {
+    // Envs of more than one warp keep the smallest CTA: more, narrower CTAs
+    // measured faster (us/step run / step, smallest CTA vs grown to 7-8 warps
+    // with 2 envs): discrete A = 100 30.3 / 31.4 vs 33.1 / 33.8, continuous
+    // A = 100 41.6 / 46.8 vs 46.9 / 50.2. At A = 20 it was mixed (continuous
+    // 9.1 / 14.1 vs 8.7 / 14.5) and discrete A = 10 gains from growing (9.3 at
+    // two warps vs 9.8 at one), so warp-sized envs still grow.
+    const int wmax = static_cast<int>(std::clamp<int64_t>(tuning("packed_warps_max", A > 32 ? 1 : 8), 1, 8));
+    for (int cand = w; cand <= std::min(wmax, kMaxThreadsPerCta / 32); cand *= 2) {
       const int64_t epc = (32 * cand) / A;
       const int64_t ctas = (store.num_envs() + epc - 1) / epc;
       if (cand == w || ctas >= 2 * kNumSMs) w = cand;

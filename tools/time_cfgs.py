@@ -10,7 +10,7 @@ import paper_2108_13976_b200 as W  # noqa: E402
 SHAPES = {
     "c2": (W.DISCRETE, 1000, 5, 2000), "d500": (W.DISCRETE, 500, 5, 2000), "d100": (W.DISCRETE, 100, 5, 2000),
     "c1000": (W.CONTINUOUS, 1000, 5, 2000), "c300": (W.CONTINUOUS, 300, 5, 2000),
-    "c100": (W.CONTINUOUS, 100, 5, 2000), "c150": (W.CONTINUOUS, 150, 5, 2000), "c20": (W.CONTINUOUS, 20, 5, 2000),
+    "c100": (W.CONTINUOUS, 100, 5, 2000), "c150": (W.CONTINUOUS, 150, 5, 2000), "c20": (W.CONTINUOUS, 20, 5, 2000), "c20f": (W.CONTINUOUS, 20, 0, 2000), "d20": (W.DISCRETE, 20, 5, 2000),
     "d200": (W.DISCRETE, 200, 5, 2000), "d300": (W.DISCRETE, 300, 5, 2000), "d700": (W.DISCRETE, 700, 5, 2000), "d600": (W.DISCRETE, 600, 5, 2000),
     "c500": (W.CONTINUOUS, 500, 5, 2000),
     "c2_e1776": (W.DISCRETE, 1000, 5, 1776), "c2_e2368": (W.DISCRETE, 1000, 5, 2368),

@@ -32,15 +32,14 @@ def time_shape(var, A, K, E, steps=100):
 
 
 SCANS = [
-    # discrete lattice shapes after the paired key insertion (thread cap per env)
-    ("disc500", (W.DISCRETE, 500, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
-    ("disc600", (W.DISCRETE, 600, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
-    ("disc700", (W.DISCRETE, 700, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
-    ("disc800", (W.DISCRETE, 800, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
-    ("disc900", (W.DISCRETE, 900, 5, 2000), "combo", [None, {'threads_per_env_max': 128}, {'threads_per_env_max': 160}]),
-    ("cont500", (W.CONTINUOUS, 500, 5, 2000), "combo", [None, {"threads_per_env_max": 128}]),
-    ("cont700", (W.CONTINUOUS, 700, 5, 2000), "combo", [None, {"threads_per_env_max": 128}, {"threads_per_env_max": 192}]),
-    ("cont1000", (W.CONTINUOUS, 1000, 5, 2000), "combo", [None, {"threads_per_env_max": 128}, {"threads_per_env_max": 192}]),
+    # packed (brute-force) CTA width
+    ("disc100", (W.DISCRETE, 100, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
+    ("disc150", (W.DISCRETE, 150, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
+    ("disc10", (W.DISCRETE, 10, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
+    ("cont100", (W.CONTINUOUS, 100, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
+    ("cont20", (W.CONTINUOUS, 20, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
+    ("cont150", (W.CONTINUOUS, 150, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
+    ("cont1000", (W.CONTINUOUS, 1000, 5, 2000), "combo", [None]),
 ]
 for name, shape, key, vals in SCANS:
     for v in vals:
