@@ -32,14 +32,14 @@ def time_shape(var, A, K, E, steps=100):
 
 
 SCANS = [
-    # packed (brute-force) CTA width
-    ("disc100", (W.DISCRETE, 100, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
-    ("disc150", (W.DISCRETE, 150, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
-    ("disc10", (W.DISCRETE, 10, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
-    ("cont100", (W.CONTINUOUS, 100, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
-    ("cont20", (W.CONTINUOUS, 20, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
-    ("cont150", (W.CONTINUOUS, 150, 5, 2000), "packed_warps_max", [8, 4, 2, 1]),
-    ("cont1000", (W.CONTINUOUS, 1000, 5, 2000), "combo", [None]),
+    # re-tuning after the K-NN changes: lattice vs brute, thread caps, staging rows
+    ("disc100", (W.DISCRETE, 100, 5, 2000), "combo", [None, {"brute_max": 64}]),
+    ("disc128", (W.DISCRETE, 128, 5, 2000), "combo", [None, {"brute_max": 64}, {"brute_max": 256}]),
+    ("disc160", (W.DISCRETE, 160, 5, 2000), "combo", [None, {"brute_max": 64}, {"brute_max": 256}]),
+    ("disc200", (W.DISCRETE, 200, 5, 2000), "combo", [None, {"brute_max": 256}]),
+    ("cont300", (W.CONTINUOUS, 300, 5, 2000), "combo", [None, {"threads_per_env_max": 192}, {"stage_rows": 32}]),
+    ("cont400", (W.CONTINUOUS, 400, 5, 2000), "combo", [None, {"threads_per_env_max": 192}]),
+    ("cont1000", (W.CONTINUOUS, 1000, 5, 2000), "combo", [None, {"stage_rows": 32}]),
 ]
 for name, shape, key, vals in SCANS:
     for v in vals:
