@@ -311,6 +311,7 @@ class Rollout {
   uint64_t h_actions0_ = 0;
   uint32_t* pdl_flags_ = nullptr;  // the store's (DataStore::pdl_flags)
   bool graph_pdl_ = false;         // the captured graph's nodes overlap (PDL)
+  bool graph_plain_pdl_ = false;   // ... through plain PDL (no per-env flags)
   void set_pdl(TagLaunch& L, bool single_step) const;
   void note_launch(const TagLaunch& L);
   // host-driven stepping: double-buffered logits, H2D and D2H copy streams,

@@ -1266,6 +1266,16 @@ void Rollout::build_graph() {
   }
   const int graph_mode = plan_.pdl_mode();
   graph_pdl_ = pol_[0] == nullptr && pdl_flags_ != nullptr && graph_mode != 0 && graph_mode != 3;
+  // Plain PDL between the captured nodes (programmatic edges, whole-grid
+  // griddepcontrol.wait, no flags) for the plans whose direct launches use it
+  // (pdl_mode 3: packed small envs such as C4), when the grid holds at most
+  // one warp per SM scheduler. C4 single-step replay, us/step with / without
+  // (4096-step windows, tools/c4_graph_ab.py): E = 1 4.14 / 4.54, 1000 4.50 /
+  // 4.78, 2000 4.61 / 4.88, 3000 4.68 / 4.87 (500 warps); 5000 5.13 / 5.02
+  // (834 warps), 7000 5.37 / 5.13, 10000 5.92 / 5.45.
+  const TagDevConfig& gd = plan_.dev();
+  graph_plain_pdl_ = pol_[0] == nullptr && pdl_flags_ != nullptr && graph_mode == 3 &&
+                     static_cast<int64_t>(gd.grid_ctas) * gd.threads / 32 <= 4 * kNumSMs;
   cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
   cudaError_t err = cudaSuccess;
   for (int i = 0; i < kGraphSteps && err == cudaSuccess; ++i) {
@@ -1281,6 +1291,7 @@ void Rollout::build_graph() {
     L.step_dev = step_dev_;
     L.step_add = i;
     L.action_h0 = h_actions0_;
+    if (graph_plain_pdl_) L.pdl_wait = 1;
     if (graph_pdl_) {  // overlapped nodes (programmatic edges)
       L.env_seq = pdl_flags_;
       L.seq_dev = step_dev_ + 1;
@@ -1344,7 +1355,9 @@ void Rollout::run(int64_t steps) {
       cuda_check(cudaGraphLaunch(graph_exec_, store_.stream()), "graph launch");
       if (graph_pdl)
         for (int i = 0; i < kGraphSteps; ++i) store_.commit_pdl_seq();
-      store_.set_pdl_open(false);  // the last node is a Tag launch that either publishes or never releases early
+      // the last node is a Tag launch that publishes its flags, never releases
+      // early, or (plain PDL) releases early without flags
+      store_.set_pdl_open(graph_plain_pdl_);
       launches_ += 1 + kGraphSteps * (pol_[0] != nullptr ? (pol_[0] == pol_[1] ? 2 : 3) : 1);
       t_ += kGraphSteps;
       steps -= kGraphSteps;

@@ -542,30 +542,42 @@ def test_cpp_facade_example(tmp_path):
     assert "env_steps=640" in r.stdout
 
 
+@pytest.mark.parametrize("multistep", [-1, 0])
 @pytest.mark.parametrize("kw,envs", [(dict(num_taggers=1, num_runners=4), 300),
+                                     (dict(num_taggers=1, num_runners=4), 6000),
                                      (dict(num_taggers=20, num_runners=80, obs_mode=O.PARTIAL,
                                            grid_size=10, episode_length=15), 37)])
-def test_graph_replay_equals_direct_launches(kw, envs):
+def test_graph_replay_equals_direct_launches(kw, envs, multistep):
     """RolloutDriver::run replays a captured CUDA graph of fused launches whose
     step index is read on device; it must equal step-by-step launches and the
-    oracle bit-for-bit, across window boundaries (53 = 3 x 16 + 5)."""
+    oracle bit-for-bit, across window boundaries (53 = 3 x 16 + 5), then
+    continue with direct steps. multistep=0 forces the graph path on the C4
+    shapes (plain PDL edges between the nodes at 300 envs, none at 6000)."""
     dc, oc = cfg_pair(**kw)
-    ws1, ws2 = W.Workspace(dc, envs), W.Workspace(dc, envs)
-    d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 9)
-    d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 9)
-    d2.set_graphs(False)
-    d1.run(53)
-    for _ in range(53):
-        d2.step()
-    assert d1.next_step() == d2.next_step() == 53
-    names = O.array_layout(oc, envs).keys()
-    assert O.first_divergence(dev_snapshot(ws1, names), dev_snapshot(ws2, names)) is None
-    o = O.OracleWorld(oc, envs)
-    o.rollout(0, 53, 9)
-    assert_same(dev_snapshot(ws1, names), o.snapshot(), "graph replay")
-    np.testing.assert_array_equal(d1.stats()[:5], o.stats()[:5])
-    ws1.close()
-    ws2.close()
+    W.set_tuning("multistep", multistep)
+    try:
+        ws1, ws2 = W.Workspace(dc, envs), W.Workspace(dc, envs)
+        d1 = W.RolloutDriver(ws1.store, ws1.plan, ws1.resets, 9)
+        d2 = W.RolloutDriver(ws2.store, ws2.plan, ws2.resets, 9)
+        d2.set_graphs(False)
+        d1.run(53)
+        d1.step()
+        d1.run(32)
+        for _ in range(86):
+            d2.step()
+        assert d1.next_step() == d2.next_step() == 86
+        names = O.array_layout(oc, envs).keys()
+        assert O.first_divergence(dev_snapshot(ws1, names), dev_snapshot(ws2, names)) is None
+        if envs <= 300:
+            o = O.OracleWorld(oc, envs)
+            o.rollout(0, 86, 9)
+            assert_same(dev_snapshot(ws1, names), o.snapshot(), "graph replay")
+            np.testing.assert_array_equal(d1.stats()[:5], o.stats()[:5])
+        d1.check()
+        ws1.close()
+        ws2.close()
+    finally:
+        W.set_tuning("multistep", -1)
 
 
 @pytest.mark.parametrize("kw,envs", [
