@@ -255,7 +255,8 @@ WDG_API wdg_status wdg_rollout_set_overlap(wdg_rollout* rollout, int32_t enabled
 /* Plan tuning overrides for A/B measurements and path-pinning tests: how a
  * plan maps the step onto the GPU, never what it computes. Keys:
  * stage_rows, brute_max, threads_per_env_max, cont_cell_div, disc_grid_cells,
- * stage_obs, bulk_in, l2_prefetch, pdl_mode, multistep; value < 0 restores
+ * stage_obs, bulk_in, l2_prefetch, pdl_mode, multistep, cont_keys,
+ * packed_warps_max; value < 0 restores
  * the plan's own choice; key "reset" restores all. Read when a plan is built
  * (geometry) or a rollout launches (pdl_mode, multistep). */
 WDG_API wdg_status wdg_set_tuning(const char* key, int64_t value);

@@ -124,3 +124,21 @@ def test_cpp_facade_builds_and_fails_loudly_without_gpu(tmp_path):
         pytest.skip("GPU present: the run is covered by test_parity_gpu")
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 2 and "no CUDA device" in r.stderr
+
+
+def test_tuning_keys_documented_and_accepted():
+    """Every plan tuning key the header lists is accepted by wdg_set_tuning
+    (host-side table, no device), an unknown key is an error, and "reset"
+    restores the plan's own choices."""
+    text = open(HEADER).read()
+    block = text[text.index("Plan tuning overrides"):text.index("WDG_API wdg_status wdg_set_tuning")]
+    keys = re.findall(r"\b([a-z][a-z0-9]*(?:_[a-z0-9]+)+|multistep)\b", block.split("Keys:")[1].split(";")[0])
+    assert {"brute_max", "cont_keys", "packed_warps_max", "pdl_mode", "multistep"} <= set(keys)
+    try:
+        for k in keys:
+            W.set_tuning(k, 1)
+            W.set_tuning(k, -1)
+        with pytest.raises(Exception):
+            W.set_tuning("no_such_key", 1)
+    finally:
+        W.set_tuning("reset")
